@@ -1,0 +1,147 @@
+/*
+ * fbgpu.h — C ABI of the B200-native GPA (Gaussian-polynomial) bilateral filter.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `fastbilateral` 0.1.0 (pure Python/numpy).  The reference has no FFI of its
+ * own; its seam is the Python function `gpa_filter`
+ * (/root/reference/pkg/src/fastbilateral/engine.py:27-80).  Every entry point
+ * below names the reference function it replaces.  Plain pointers and sizes
+ * only — no torch or numpy types cross this boundary.  A ctypes binding lives
+ * in paper_1603_08109_b200/_native.py; INTEGRATION.md shows the stub a
+ * reference maintainer would add.
+ *
+ * Conventions
+ *   - Every function returns an fb_status (0 = FB_OK).  On failure
+ *     fb_last_error() returns a thread-local, human-readable message.
+ *   - Images are row-major 2-D arrays with a leading dimension `ld`
+ *     (elements), resident on the host (`on_device = 0`, any host memory;
+ *     pinned memory makes the copies asynchronous) or on the context's device.
+ *   - Calls are synchronous at return (results and fb_stats are final);
+ *     the work inside is stream-ordered on the context's stream.
+ *   - A context owns its device workspace, is bound to one device and is not
+ *     re-entrant; distinct contexts may be driven from distinct host threads.
+ */
+#ifndef FBGPU_H
+#define FBGPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FBGPU_VERSION 100 /* 1.0.0 */
+
+typedef struct fb_ctx fb_ctx;
+
+typedef enum fb_dtype {
+  FB_U8 = 0,  /* 8-bit unsigned samples (e.g. a loaded PGM) */
+  FB_F32 = 1, /* float32 */
+  FB_F64 = 2  /* float64 (the reference's image type, image.py:35-42) */
+} fb_dtype;
+
+typedef enum fb_kind {
+  FB_BOX = 0,      /* box_filter, conv.py:43-54 */
+  FB_GAUSSIAN = 1  /* separable truncated Gaussian, conv.py:57-80 */
+} fb_kind;
+
+typedef enum fb_precision {
+  FB_PREC_F32 = 1, /* fp32 channels/accumulation (performance configs) */
+  FB_PREC_F64 = 2  /* fp64 throughout (small images, sigma_r < 16) */
+} fb_precision;
+
+typedef enum fb_status {
+  FB_OK = 0,
+  FB_ERR_PARAM = 1,            /* -> ParameterError (errors.py:4-5) */
+  FB_ERR_NONFINITE_INPUT = 2,  /* -> ParameterError "image contains non-finite samples" (image.py:40-41) */
+  FB_ERR_RANGE = 3,            /* -> RangeViolationError (image.py:45-54) */
+  FB_ERR_NUMERIC = 4,          /* -> NumericRangeError (engine.py:73-76) */
+  FB_ERR_WINDOW = 5,           /* -> ParameterError "window half-width W too large" (conv.py:19-27) */
+  FB_ERR_CUDA = 6,             /* CUDA runtime failure */
+  FB_ERR_NOMEM = 7             /* device allocation failed */
+} fb_status;
+
+typedef struct fb_image {
+  void* data;        /* first element */
+  int32_t dtype;     /* fb_dtype */
+  int32_t on_device; /* 0 = host memory, 1 = device memory of the context's device */
+  int64_t rows;
+  int64_t cols;
+  int64_t ld;        /* elements between consecutive rows (>= cols) */
+} fb_image;
+
+typedef struct fb_spatial {
+  int32_t kind;              /* fb_kind */
+  int32_t half_width;        /* W (box: half-width; gaussian: ceil(3 sigma_s)) */
+  const double* weights_1d;  /* 2W+1 normalised taps (gaussian; ignored for box), kernels.py:81-85 */
+} fb_spatial;
+
+typedef struct fb_stats {
+  int64_t spatial_filter_calls; /* N+1 (engine.py:77-79) */
+  int64_t order;                /* N */
+  int64_t degenerate_pixels;    /* pixels that hit the |Q| < 1e-30 pass-through (engine.py:68-72) */
+  int64_t nonfinite_outputs;    /* non-finite outputs (-> FB_ERR_NUMERIC) */
+  int64_t bad_index;            /* row-major index (in the input buffer) of the first offending sample */
+  double bad_value;             /* its value */
+  double device_ms;             /* device time of the whole call (CUDA events), incl. copies */
+  double kernel_ms;             /* device time of the filter kernels only */
+  int64_t h2d_bytes;
+  int64_t d2h_bytes;
+  int32_t bands;                /* row bands the workspace limit split the image into */
+  int32_t precision;            /* fb_precision actually used */
+  int64_t launches;             /* kernels launched by this call */
+} fb_stats;
+
+/* Context lifecycle (the reference is stateless; the context is where the
+ * "allocated once" workspace of SPEC.md:383 lives). */
+int fb_create(int device, fb_ctx** out);
+int fb_destroy(fb_ctx* ctx);
+/* Use an existing cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL = the context's own. */
+int fb_set_stream(fb_ctx* ctx, void* cuda_stream);
+/* Upper bound for the channel-plane workspace (bytes); the image is processed in row bands below it. */
+int fb_set_workspace_limit(fb_ctx* ctx, int64_t bytes);
+
+/*
+ * fb_gpa_filter — replaces gpa_filter (engine.py:27-80): Algorithm 2 with an
+ * explicit order N >= 1.  Channel generation + vertical pass (kernel 1) and
+ * horizontal pass + Horner epilogue + divide (kernel 2) on the device.
+ *
+ * `in` may carry `halo_top` / `halo_bottom` extra rows above/below the rows to
+ * filter (row-band partitioning across GPUs: neighbour rows exchanged over
+ * NVLink).  Output rows = in->rows - halo_top - halo_bottom; rows outside the
+ * buffer are replicated from its first/last row (the reference's edge pad).
+ * Only the output rows are checked for finiteness / range [center -
+ * half_range, center + half_range] (image.py:35-54).
+ * `out` must be FB_F32 or FB_F64 (the reference returns float64).
+ * The caller validates sigma_r and the order (engine.py:40-49) and the box
+ * window (conv.py:19-27); they are re-checked here and reported as FB_ERR_PARAM.
+ */
+int fb_gpa_filter(fb_ctx* ctx, const fb_image* in, int64_t halo_top, int64_t halo_bottom,
+                  fb_image* out, const fb_spatial* spatial, double sigma_r, int32_t order,
+                  double center, double half_range, int32_t precision, fb_stats* stats);
+
+/*
+ * fb_spatial_filter — replaces apply_spatial / box_filter / gaussian_filter
+ * (conv.py:43-80): one normalised box or separable Gaussian filtering with
+ * replicate boundary.  Inputs must be finite (FB_ERR_NONFINITE_INPUT otherwise).
+ */
+int fb_spatial_filter(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_spatial* spatial,
+                      int32_t precision, fb_stats* stats);
+
+/*
+ * fb_validate — replaces as_image's finiteness check + validate_range
+ * (image.py:35-54) without filtering: FB_ERR_NONFINITE_INPUT / FB_ERR_RANGE
+ * with stats->bad_index / bad_value of the first offending sample.
+ */
+int fb_validate(fb_ctx* ctx, const fb_image* in, double lo, double hi, fb_stats* stats);
+
+/* Message of the last failure on this host thread. */
+const char* fb_last_error(void);
+int fb_version(void);
+/* Number of kernels this library has launched in this process (for launch accounting). */
+int64_t fb_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FBGPU_H */

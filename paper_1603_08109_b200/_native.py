@@ -1,0 +1,209 @@
+"""ctypes binding of the C ABI in `include/fbgpu.h` (libfbgpu.so, built in-tree).
+
+This is the only place the package touches native code.  There is no CPU
+fallback: if the library is missing or no CUDA device is usable, every
+filtering call raises `NativeError`.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from .errors import NativeError, NumericRangeError, ParameterError, RangeViolationError
+from .image import range_message
+
+LIB_NAME = "libfbgpu.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+FB_U8, FB_F32, FB_F64 = 0, 1, 2
+FB_BOX, FB_GAUSSIAN = 0, 1
+FB_PREC_F32, FB_PREC_F64 = 1, 2
+(FB_OK, FB_ERR_PARAM, FB_ERR_NONFINITE_INPUT, FB_ERR_RANGE, FB_ERR_NUMERIC, FB_ERR_WINDOW,
+ FB_ERR_CUDA, FB_ERR_NOMEM) = range(8)
+
+#: Every symbol include/fbgpu.h declares (checked by tests/test_native_abi.py).
+EXPORTED_SYMBOLS = (
+    "fb_create", "fb_destroy", "fb_set_stream", "fb_set_workspace_limit", "fb_gpa_filter",
+    "fb_spatial_filter", "fb_validate", "fb_last_error", "fb_version", "fb_launch_count",
+)
+
+
+class FbImage(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("dtype", ctypes.c_int32), ("on_device", ctypes.c_int32),
+                ("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("ld", ctypes.c_int64)]
+
+
+class FbSpatial(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("half_width", ctypes.c_int32),
+                ("weights_1d", ctypes.POINTER(ctypes.c_double))]
+
+
+class FbStats(ctypes.Structure):
+    _fields_ = [("spatial_filter_calls", ctypes.c_int64), ("order", ctypes.c_int64),
+                ("degenerate_pixels", ctypes.c_int64), ("nonfinite_outputs", ctypes.c_int64),
+                ("bad_index", ctypes.c_int64), ("bad_value", ctypes.c_double),
+                ("device_ms", ctypes.c_double), ("kernel_ms", ctypes.c_double),
+                ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
+                ("bands", ctypes.c_int32), ("precision", ctypes.c_int32), ("launches", ctypes.c_int64)]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+_lib = None
+_lib_lock = threading.Lock()
+_contexts: dict[int, ctypes.c_void_p] = {}
+
+
+def load_library(path: str | None = None) -> ctypes.CDLL:
+    """Load libfbgpu.so (once).  Raises NativeError when it has not been built."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None:
+            return _lib
+        path = path or LIB_PATH
+        if not os.path.exists(path):
+            raise NativeError(f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        lib = ctypes.CDLL(path)
+        P = ctypes.POINTER
+        vp = ctypes.c_void_p
+        lib.fb_create.argtypes = [ctypes.c_int, P(vp)]
+        lib.fb_destroy.argtypes = [vp]
+        lib.fb_set_stream.argtypes = [vp, vp]
+        lib.fb_set_workspace_limit.argtypes = [vp, ctypes.c_int64]
+        lib.fb_gpa_filter.argtypes = [vp, P(FbImage), ctypes.c_int64, ctypes.c_int64, P(FbImage), P(FbSpatial),
+                                      ctypes.c_double, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_int32, P(FbStats)]
+        lib.fb_spatial_filter.argtypes = [vp, P(FbImage), P(FbImage), P(FbSpatial), ctypes.c_int32, P(FbStats)]
+        lib.fb_validate.argtypes = [vp, P(FbImage), ctypes.c_double, ctypes.c_double, P(FbStats)]
+        lib.fb_last_error.restype = ctypes.c_char_p
+        lib.fb_version.restype = ctypes.c_int
+        lib.fb_launch_count.restype = ctypes.c_int64
+        for name in ("fb_create", "fb_destroy", "fb_set_stream", "fb_set_workspace_limit", "fb_gpa_filter",
+                     "fb_spatial_filter", "fb_validate"):
+            getattr(lib, name).restype = ctypes.c_int
+        _lib = lib
+        return lib
+
+
+def context(device: int = 0) -> ctypes.c_void_p:
+    """The per-device context (created on first use, owns the device workspace)."""
+    lib = load_library()
+    with _lib_lock:
+        ctx = _contexts.get(device)
+        if ctx is None:
+            ctx = ctypes.c_void_p()
+            rc = lib.fb_create(device, ctypes.byref(ctx))
+            if rc != FB_OK:
+                raise NativeError(f"fb_create(device={device}) failed: {lib.fb_last_error().decode()}")
+            _contexts[device] = ctx
+        return ctx
+
+
+def launch_count() -> int:
+    return int(load_library().fb_launch_count())
+
+
+def set_workspace_limit(nbytes: int, device: int = 0) -> None:
+    lib = load_library()
+    _check(lib, lib.fb_set_workspace_limit(context(device), int(nbytes)), None, None)
+
+
+# ----------------------------------------------------------------------------- arrays
+_NP_DT = {np.dtype(np.uint8): FB_U8, np.dtype(np.float32): FB_F32, np.dtype(np.float64): FB_F64}
+_TORCH_DT = {"torch.uint8": FB_U8, "torch.float32": FB_F32, "torch.float64": FB_F64}
+
+
+def is_cuda_tensor(x) -> bool:
+    return type(x).__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def image_desc(arr) -> FbImage:
+    """fb_image for a 2-D numpy array (host) or CUDA torch tensor (device); rows must be unit-stride."""
+    if is_cuda_tensor(arr):
+        rs, cs = arr.stride()
+        if cs != 1:
+            raise ValueError("tensor rows must be contiguous")
+        return FbImage(arr.data_ptr(), _TORCH_DT[str(arr.dtype)], 1, arr.shape[0], arr.shape[1], rs)
+    isz = arr.itemsize
+    if arr.strides[1] != isz or arr.strides[0] % isz or arr.strides[0] < arr.shape[1] * isz:
+        raise ValueError("array rows must be contiguous")
+    return FbImage(arr.ctypes.data, _NP_DT[arr.dtype], 0, arr.shape[0], arr.shape[1], arr.strides[0] // isz)
+
+
+def spatial_desc(kernel):
+    taps = np.ascontiguousarray(kernel.weights_1d, dtype=np.float64)
+    kind = FB_BOX if kernel.kind == "box" else FB_GAUSSIAN
+    return FbSpatial(kind, int(kernel.half_width), taps.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), taps
+
+
+def _check(lib, rc: int, src, stats: FbStats | None, lo=None, hi=None):
+    """Translate a status code into the reference's exception (same classes and messages)."""
+    if rc == FB_OK:
+        return
+    msg = lib.fb_last_error().decode(errors="replace")
+    if rc == FB_ERR_NONFINITE_INPUT:
+        raise ParameterError("image contains non-finite samples")
+    if rc == FB_ERR_RANGE:
+        cols = src.shape[1]
+        row, col = divmod(int(stats.bad_index), cols)
+        raise RangeViolationError(range_message(np.float64(stats.bad_value), row, col, lo, hi))
+    if rc in (FB_ERR_PARAM, FB_ERR_WINDOW):
+        raise ParameterError(msg)
+    if rc == FB_ERR_NUMERIC:
+        raise NumericRangeError(msg)
+    raise NativeError(f"libfbgpu: {msg} (status {rc})")
+
+
+def _stream_for(arr, device: int):
+    if is_cuda_tensor(arr):
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream(arr.device).cuda_stream)
+    return ctypes.c_void_p(None)
+
+
+def device_of(arr, device: int | None) -> int:
+    if is_cuda_tensor(arr):
+        return arr.device.index or 0
+    return 0 if device is None else int(device)
+
+
+def gpa(src, out, kernel, sigma_r: float, order: int, center: float, half_range: float, precision: int,
+        device: int = 0, halo_top: int = 0, halo_bottom: int = 0) -> dict:
+    """Run fb_gpa_filter; `src`/`out` are numpy arrays or CUDA tensors. Returns the stats dict."""
+    lib = load_library()
+    ctx = context(device)
+    lib.fb_set_stream(ctx, _stream_for(src, device))
+    sp, _taps = spatial_desc(kernel)
+    st = FbStats()
+    rc = lib.fb_gpa_filter(ctx, ctypes.byref(image_desc(src)), halo_top, halo_bottom, ctypes.byref(image_desc(out)),
+                           ctypes.byref(sp), float(sigma_r), int(order), float(center), float(half_range),
+                           int(precision), ctypes.byref(st))
+    _check(lib, rc, src, st, center - half_range, center + half_range)
+    return st.as_dict()
+
+
+def spatial(src, out, kernel, precision: int, device: int = 0) -> dict:
+    lib = load_library()
+    ctx = context(device)
+    lib.fb_set_stream(ctx, _stream_for(src, device))
+    sp, _taps = spatial_desc(kernel)
+    st = FbStats()
+    rc = lib.fb_spatial_filter(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)), ctypes.byref(sp),
+                               int(precision), ctypes.byref(st))
+    _check(lib, rc, src, st)
+    return st.as_dict()
+
+
+def validate(src, lo: float, hi: float, device: int = 0) -> None:
+    """Device-side as_image finiteness + validate_range; raises like the reference."""
+    lib = load_library()
+    ctx = context(device)
+    lib.fb_set_stream(ctx, _stream_for(src, device))
+    st = FbStats()
+    rc = lib.fb_validate(ctx, ctypes.byref(image_desc(src)), float(lo), float(hi), ctypes.byref(st))
+    _check(lib, rc, src, st, lo, hi)

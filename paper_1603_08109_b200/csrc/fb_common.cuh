@@ -1,0 +1,101 @@
+// fb_common.cuh — shared device helpers and the kernel argument block.
+//
+// Data layout in HBM:
+//   input f      : row-major, leading dim f_ld, dtype u8/f32/f64, rows_in rows
+//                  (rows [halo_top, rows_in - halo_bottom) are the rows to filter)
+//   channel planes v : T[N+1][band_rows_max][pitch], pitch = round_up(cols + 2W, 32).
+//                  Plane n holds the VERTICALLY filtered channel c_n = e x^n / sqrt(n!)
+//                  of the current row band, with W replicate columns on each side
+//                  (padded column pc <-> image column clamp(pc - W, 0, cols-1)),
+//                  so the horizontal pass never leaves the plane.
+//   output       : row-major f32/f64, leading dim out_ld.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fbgpu {
+
+constexpr int kMaxW = 160;                  // largest half-width the kernels accept
+constexpr int kMaxTaps = 2 * kMaxW + 1;
+
+enum : int { kModeGpa = 0, kModePlain = 1 };
+enum : int { kKindBox = 0, kKindGauss = 1 };
+enum : int { kFlagFirstNonfinite = 0, kFlagFirstRange = 1, kFlagDegenerate = 2, kFlagNonfiniteOut = 3 };
+
+template <typename T>
+struct GpaArgs {
+  // input buffer
+  const void* f;
+  long long f_ld;
+  int f_dtype;        // 0 u8, 1 f32, 2 f64
+  int rows_in;        // rows in the buffer (incl. halos)
+  int cols;
+  int halo_top;       // buffer row of output row 0
+  // current row band
+  int band_row0;      // first output row of the band
+  int band_rows;      // output rows in the band
+  // channel planes (workspace)
+  T* v;
+  long long pitch;    // elements per plane row
+  long long plane;    // elements per plane
+  int wpad;           // cols + 2W  (valid padded columns)
+  // filter
+  int W;
+  int N;
+  int mode;           // kModeGpa / kModePlain
+  int check;          // validate input samples of the band
+  double tc;          // range centre t_c
+  double inv_sr;      // 1 / sigma_r
+  double sr;          // sigma_r
+  double lo, hi;      // declared range
+  T norm;             // box: 1/(2W+1)^2, gaussian: 1
+  // output
+  void* out;
+  long long out_ld;
+  int out_dtype;      // 1 f32, 2 f64
+  unsigned long long* flags;
+  T w[kMaxTaps];      // normalised 1-D taps (gaussian)
+};
+
+__device__ __forceinline__ double load_sample(const void* f, int dt, long long idx) {
+  if (dt == 1) return (double)__ldg(reinterpret_cast<const float*>(f) + idx);
+  if (dt == 2) return __ldg(reinterpret_cast<const double*>(f) + idx);
+  return (double)__ldg(reinterpret_cast<const unsigned char*>(f) + idx);
+}
+
+__device__ __forceinline__ void store_sample(void* out, int dt, long long idx, double v) {
+  if (dt == 2) reinterpret_cast<double*>(out)[idx] = v;
+  else reinterpret_cast<float*>(out)[idx] = (float)v;
+}
+
+template <typename T> __device__ __forceinline__ T gauss_exp(T x);
+template <> __device__ __forceinline__ float gauss_exp<float>(float x) { return expf(-0.5f * x * x); }
+template <> __device__ __forceinline__ double gauss_exp<double>(double x) { return exp(-0.5 * x * x); }
+
+__device__ __forceinline__ bool finite_d(double v) { return isfinite(v); }
+
+// Record the smallest row-major index of an offending input sample:
+// warp-aggregated so a fully invalid image costs one atomic per warp.
+__device__ __forceinline__ void flag_min(unsigned long long* slot, bool bad, unsigned long long idx) {
+  unsigned mask = __ballot_sync(0xffffffffu, bad);
+  if (!mask) return;
+  unsigned long long v = bad ? idx : ~0ull;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long u = __shfl_xor_sync(0xffffffffu, v, o);
+    v = u < v ? u : v;
+  }
+  if ((threadIdx.x & 31) == (__ffs(mask) - 1)) atomicMin(slot, v);
+}
+
+// Validate one input sample (finite first, then declared range), as
+// as_image + validate_range do (image.py:35-54).
+__device__ __forceinline__ void check_sample(unsigned long long* flags, bool active, double fv,
+                                             double lo, double hi, unsigned long long idx) {
+  bool nonfinite = active && !isfinite(fv);
+  bool outside = active && (fv < lo || fv > hi);
+  flag_min(flags + kFlagFirstNonfinite, nonfinite, idx);
+  flag_min(flags + kFlagFirstRange, outside, idx);
+}
+
+}  // namespace fbgpu
