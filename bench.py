@@ -1,0 +1,433 @@
+"""Benchmark of the GPA bilateral filter hot path (one JSON line on rank 0).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+A "step" is one pass of the filter over the config's whole workload:
+  c4 (default): one 16384^2 float32 image, box W=20, sigma_r=25, delta=1 -> N=57;
+                at N>1 GPUs: row bands + P2P halo exchange + gather to rank 0.
+  c3: 64 float32 images of 2048^2, Gaussian sigma_s=8, sigma_r=20, delta=1 -> N=76; by image.
+  c0/c1/c2: single images (replicas at N>1).
+`value` = megapixels/s over all ranks with inputs resident in HBM (device
+events, max over ranks); `e2e` = the same metric through the public API with
+host buffers (H2D of the input and D2H of the float64 result inside the timed
+region).  Inputs are larger than L2 (126 MB) for c2-c4 and the channel
+workspace is several GB, so no L2 flush is needed there; c0/c1 flush L2
+between steps.  `--impl reference` times the CPU restatement of the
+reference algorithm (oracle/, numpy fp64) on all host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1603_08109_b200 import synth  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12  # 74.4; FFMA probe measured 72-74 (profiles/)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-mp", type=float, default=0.0, help="override the CPU sample size (MP)")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks():
+    try:
+        with open(PEAKS_FILE) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms while the timed region runs."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[2:6]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic_bytes(cfg, N):
+    """Per pixel: B_alg = 2 s_io + 2 (N+1) 4 and the split over the two kernels."""
+    s_in = np.dtype(cfg.dtype).itemsize
+    s_out = 4  # device-resident runs write float32
+    ch = (N + 1) * 4
+    return {"pipeline": s_in + s_out + 2 * ch, "k1": s_in + ch, "k2": ch + s_in + s_out}
+
+
+def algorithmic_flops(cfg, N):
+    """FP32 FLOPs per pixel of the two kernels (FMA = 2): taps per pass x channels + Horner."""
+    W = synth.config_kernel(cfg).half_width
+    if cfg.kind == "box":
+        per_pass = 2  # running sum: one add, one subtract
+    else:
+        per_pass = 2 * (2 * W + 1)
+    return {"k1": (N + 1) * (per_pass + 2), "k2": (N + 1) * (per_pass + 6)}
+
+
+def ncu_traffic(config, kernel):
+    """dram bytes per launch for `kernel` from the committed ncu summary of this config, else None."""
+    path = os.path.join(ROOT, "profiles", f"ncu_{config}.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d["kernels"][kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- reference arm (CPU)
+_CPU_IMG = None  # shared with forked workers (no per-job pickling of the image)
+
+
+def _oracle_tile(args):
+    y0, y1, x0, x1, kind, W, taps, sigma_r, N = args
+    from oracle import gpa_oracle
+    img = _CPU_IMG
+    H, Wd = img.shape
+    ya, yb, xa, xb = max(0, y0 - W), min(H, y1 + W), max(0, x0 - W), min(Wd, x1 + W)
+    out = gpa_oracle.gpa(img[ya:yb, xa:xb], kind, W, taps, sigma_r, N)
+    return out[y0 - ya:y1 - ya, x0 - xa:x1 - xa]
+
+
+def cpu_sample_region(cfg, target_mp):
+    """A contiguous block of the workload of about `target_mp` megapixels (whole rows of image 0)."""
+    rows = max(64, min(cfg.height, int(target_mp * 1e6 / cfg.width)))
+    return rows, cfg.width
+
+
+def run_cpu(img, cfg, N, rows, cores):
+    """Filter the first `rows` rows of `img` with the oracle on `cores` processes; returns seconds."""
+    k = synth.config_kernel(cfg)
+    tile_r = 256
+    tile_c = min(cfg.width, 2048)
+    global _CPU_IMG
+    _CPU_IMG = np.ascontiguousarray(img[: min(cfg.height, rows + k.half_width)])
+    jobs = []
+    for y in range(0, rows, tile_r):
+        for x in range(0, cfg.width, tile_c):
+            jobs.append((y, min(rows, y + tile_r), x, min(cfg.width, x + tile_c), cfg.kind,
+                         k.half_width, k.weights_1d, cfg.sigma_r, N))
+    t0 = time.perf_counter()
+    if cores > 1:
+        import multiprocessing as mp
+        with mp.get_context("fork").Pool(cores) as pool:
+            pool.map(_oracle_tile, jobs, chunksize=1)
+    else:
+        for j in jobs:
+            _oracle_tile(j)
+    return time.perf_counter() - t0
+
+
+def reference_arm(args, cfg, N):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    img = synth.config_image(cfg)
+    # ~2 MP per core per step keeps a step near 10 s on one of these Xeons.
+    per_core_mp = 2.0 if cfg.kind == "box" else 0.8
+    target = args.cpu_sample_mp or per_core_mp * cores
+    rows, cols = cpu_sample_region(cfg, target)
+    mp_per_step = rows * cols / 1e6
+    for _ in range(args.warmup):
+        run_cpu(img, cfg, N, rows, cores)
+    times = [run_cpu(img, cfg, N, rows, cores) for _ in range(args.steps)]
+    total = sum(times)
+    value = mp_per_step * args.steps / total
+    sample = (f"first {rows} rows x {cols} cols of image 0 ({mp_per_step:.2f} MP) per step, "
+              f"tiled 256x2048 with W halos over a {cores}-process pool; numpy fp64 oracle/gpa_oracle.py")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (paper_1603_08109_b200/synth.py, seeded)", "config": config_block(cfg, N, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "MP/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+METRIC = "megapixels/sec (order N, per spatial kind) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def config_block(cfg, N, world):
+    k = synth.config_kernel(cfg)
+    par = ("by-image" if cfg.batch > 1 else ("row-bands" if cfg.name == "c4" else "replicas")) + f" x{world}"
+    l2 = "inputs+workspace > L2 (126 MB), no flush" if cfg.pixels * 4 > 126e6 else "L2 flushed between steps"
+    return {"workload": cfg.name, "image": [cfg.batch, cfg.height, cfg.width], "input_dtype": cfg.dtype,
+            "spatial": cfg.kind, "half_width": k.half_width, "sigma_s": cfg.sigma_s, "sigma_r": cfg.sigma_r,
+            "order_N": N, "delta": cfg.delta, "parallelism": par, "l2": l2}
+
+
+# ----------------------------------------------------------------------------- our arm (GPU)
+def main():
+    args = parse()
+    cfg = synth.CONFIGS[args.config]
+    N = synth.config_order(cfg)
+    if args.impl == "reference":
+        reference_arm(args, cfg, N)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1603_08109_b200 import _native, gpa_filter, sharding
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    kernel = synth.config_kernel(cfg)
+    W = kernel.half_width
+
+    # ---- this rank's share of the workload (host copies kept for e2e) --------------------
+    bands = None
+    if cfg.batch > 1:
+        idx = list(sharding.image_shard(cfg.batch, world, rank))
+        host_imgs = [synth.config_image(cfg, i) for i in idx]
+    else:
+        full = synth.config_image(cfg)
+        if world > 1 and cfg.name == "c4":
+            bands = sharding.RowBands(cfg.height, world, W)
+            r0, r1 = bands.bounds(rank)
+            host_imgs = [np.ascontiguousarray(full[r0:r1])]
+        else:
+            host_imgs = [full]
+        del full
+    dev_imgs = [torch.from_numpy(im).to(dev) for im in host_imgs]
+    dev_out = [torch.empty(im.shape, dtype=torch.float32, device=dev) for im in host_imgs]
+    my_pixels = sum(im.shape[0] * im.shape[1] for im in host_imgs)
+    root_full = None
+    if bands is not None and rank == 0:
+        root_full = torch.empty((cfg.height, cfg.width), dtype=torch.float32, device=dev)
+    flush = None
+    if cfg.pixels * 4 <= 126e6:
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    ctx_stream = torch.cuda.current_stream(dev)
+    kstats = {"k1_ms": 0.0, "k2_ms": 0.0, "kernel_ms": 0.0, "calls": 0, "launches": 0}
+
+    def step(record=False):
+        if bands is not None:
+            ext = sharding.exchange_halos(dev_imgs[0], W, rank, world, bands)
+            top, bottom = bands.halos(rank)
+            st = _native.gpa(ext, dev_out[0], kernel, cfg.sigma_r, N, 128.0, 128.0, _native.FB_PREC_F32, local,
+                             halo_top=top, halo_bottom=bottom)
+            sts = [st]
+            sharding.gather_rows(dev_out[0], root_full, rank, world, bands)
+        else:
+            sts = [_native.gpa(im, o, kernel, cfg.sigma_r, N, 128.0, 128.0, _native.FB_PREC_F32, local)
+                   for im, o in zip(dev_imgs, dev_out)]
+        if record:
+            for st in sts:
+                kstats["k1_ms"] += st["k1_ms"]
+                kstats["k2_ms"] += st["k2_ms"]
+                kstats["kernel_ms"] += st["kernel_ms"]
+                kstats["calls"] += 1
+                kstats["launches"] += st["launches"]
+
+    def timed(fn, steps):
+        ev = []
+        for _ in range(steps):
+            if flush is not None:
+                flush.zero_()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(ctx_stream)
+            fn()
+            e.record(ctx_stream)
+            ev.append((s, e))
+        torch.cuda.synchronize(dev)
+        return sum(s.elapsed_time(e) for s, e in ev)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    n_launch0 = _native.launch_count()
+    with ClockSampler(local) as clocks:
+        ms = timed(lambda: step(record=True), args.steps)
+    launches = _native.launch_count() - n_launch0
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    total_px = cfg.pixels  # every rank's share together is the whole workload
+    value = total_px * args.steps / (ms_max * 1e-3) / 1e6
+
+    # ---- e2e through the public API with host buffers ------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        pinned_in = [torch.from_numpy(im).pin_memory().numpy() for im in host_imgs]
+        pinned_out = [torch.empty(im.shape, dtype=torch.float64).pin_memory().numpy() for im in host_imgs]
+
+        def e2e_step():
+            for im, o in zip(pinned_in, pinned_out):
+                gpa_filter(im, kernel, cfg.sigma_r, N, precision="f32", device=local, out=o)
+
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        # Each call is synchronous (H2D, kernels, D2H on the context stream), so the
+        # host clock around the calls is the end-to-end time.
+        n_e2e = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            e2e_step()
+        t_ms = (time.perf_counter() - t0) * 1e3
+        t_t = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t_t, op=dist.ReduceOp.MAX)
+        e2e = {"value": total_px * n_e2e / (float(t_t.item()) * 1e-3) / 1e6, "unit": "MP/s",
+               "h2d_bytes_per_step": int(sum(im.nbytes for im in pinned_in)) * world,
+               "d2h_bytes_per_step": int(sum(o.nbytes for o in pinned_out)) * world,
+               "path": "gpa_filter(numpy pinned f32 in, out=pinned f64) per image/band; bands with halos are "
+                       "filtered per rank without exchange in this leg" if bands is not None else
+                       "gpa_filter(numpy pinned f32 in, out=pinned f64)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel --------------------------------------------------
+    hbm_peak, peak_src = peaks()
+    bpp = algorithmic_bytes(cfg, N)
+    fpp = algorithmic_flops(cfg, N)
+    calls = max(1, kstats["calls"])
+    launches_per_kernel = max(1, kstats["launches"] // 2)
+    px_call = my_pixels / len(host_imgs)
+    kernels = {}
+    for name in ("k1", "k2"):
+        t = kstats[f"{name}_ms"] / launches_per_kernel * 1e-3  # s per launch
+        px_launch = my_pixels * args.steps / launches_per_kernel
+        kernels[name] = {
+            "avg_launch_ms": t * 1e3,
+            "share_of_step": kstats[f"{name}_ms"] / max(1e-9, ms),
+            "hbm_gbs": bpp[name] * px_launch / t / 1e9,
+            "hbm_frac": bpp[name] * px_launch / t / 1e9 / hbm_peak,
+            "fp32_tflops": fpp[name] * px_launch / t / 1e12,
+            "fp32_frac": fpp[name] * px_launch / t / 1e12 / FP32_NOMINAL_TFLOPS,
+            "alg_bytes_per_px": bpp[name],
+        }
+    dom = max(("k1", "k2"), key=lambda n: kstats[f"{n}_ms"])
+    dk = kernels[dom]
+    bound = "hbm" if dk["hbm_frac"] >= dk["fp32_frac"] else "fp32"
+    kname = {"k1": "k1_gen_vpass", "k2": "k2_hpass_horner"}[dom]
+    roofline = {
+        "bound": bound, "kernel": kname,
+        "achieved": dk["hbm_gbs"] if bound == "hbm" else dk["fp32_tflops"],
+        "peak": hbm_peak if bound == "hbm" else FP32_NOMINAL_TFLOPS,
+        "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
+        "frac": dk["hbm_frac"] if bound == "hbm" else dk["fp32_frac"],
+        "traffic": ncu_traffic(cfg.name, kname),
+        "peak_source": peak_src if bound == "hbm" else "nominal 148 SM x 128 FMA/clk x 1.965 GHz",
+        "alg_bytes_per_px": dk["alg_bytes_per_px"],
+        "pipeline_hbm_frac": bpp["pipeline"] * total_px * args.steps / (ms_max * 1e-3) / 1e9 / hbm_peak,
+        "kernels": kernels,
+    }
+
+    # ---- CPU baseline (rank 0, N=1 only, bounded sample, one core) ------------------------
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        img0 = host_imgs[0] if cfg.batch > 1 or bands is None else synth.config_image(cfg)
+        target = args.cpu_sample_mp or (2.5 if cfg.kind == "box" else 1.0)
+        rows, cols = cpu_sample_region(cfg, target)
+        secs = run_cpu(img0, cfg, N, rows, 1)
+        cpu = {"value": rows * cols / 1e6 / secs, "unit": "MP/s", "cores": 1, "kind": "port",
+               "sample": f"first {rows} rows x {cols} cols of image 0 ({rows * cols / 1e6:.2f} MP), numpy fp64 "
+                         f"restatement of the reference (oracle/gpa_oracle.py), one process"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (paper_1603_08109_b200/synth.py, seeded; BASELINE recipes)",
+        "config": config_block(cfg, N, world), "clocks": clocks.summary(), "gpu_launches": launches,
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -85,6 +85,8 @@ typedef struct fb_stats {
   double bad_value;             /* its value */
   double device_ms;             /* device time of the whole call (CUDA events), incl. copies */
   double kernel_ms;             /* device time of the filter kernels only */
+  double k1_ms;                 /* of which kernel 1 (channel generation + vertical pass), summed over bands */
+  double k2_ms;                 /* of which kernel 2 (horizontal pass + Horner epilogue), summed over bands */
   int64_t h2d_bytes;
   int64_t d2h_bytes;
   int32_t bands;                /* row bands the workspace limit split the image into */

@@ -47,6 +47,7 @@ class FbStats(ctypes.Structure):
                 ("degenerate_pixels", ctypes.c_int64), ("nonfinite_outputs", ctypes.c_int64),
                 ("bad_index", ctypes.c_int64), ("bad_value", ctypes.c_double),
                 ("device_ms", ctypes.c_double), ("kernel_ms", ctypes.c_double),
+                ("k1_ms", ctypes.c_double), ("k2_ms", ctypes.c_double),
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
                 ("bands", ctypes.c_int32), ("precision", ctypes.c_int32), ("launches", ctypes.c_int64)]
 

@@ -50,10 +50,25 @@ struct fb_ctx {
   void* out_stage = nullptr;
   size_t out_stage_bytes = 0;
   unsigned long long* flags = nullptr;       // device, 4 slots
+  float* tab = nullptr;                      // device channel-constant table (fp32 fast path)
+  float* tab_host = nullptr;                 // pinned staging for it
+  int tab_cap = 0;                           // channels it holds
   unsigned long long* flags_host = nullptr;  // pinned, 8 slots (0-3 init pattern, 4-7 readback)
   long long ws_limit = 0;
   int sm_count = 148;
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // Per-band kernel boundaries: [k1 start, k1 end = k2 start, k2 end] x bands.
+  std::vector<cudaEvent_t> kev;
+  int kev_used = 0;
+
+  cudaEvent_t next_event() {
+    if (kev_used == (int)kev.size()) {
+      cudaEvent_t e = nullptr;
+      cudaEventCreate(&e);
+      kev.push_back(e);
+    }
+    return kev[kev_used++];
+  }
 };
 
 namespace {
@@ -104,27 +119,27 @@ int launch_band(fb_ctx* ctx, const Job& j, GpaArgs<T>& a, int band_row0, int ban
   a.band_rows = band_rows;
   const int W = j.W;
   bool done = false;
-  int rc = launch_fast<T>(ctx->stream, j.kind, W, a, &done);
-  if (rc != FB_OK) return rc;
+  cudaEvent_t e0 = ctx->next_event(), e1 = ctx->next_event(), e2 = ctx->next_event();
+  KernelEvents kev{e0, e1, e2};
+  int rc = launch_fast<T>(ctx->stream, j.kind, W, a, kev, &done);
+  if (rc != FB_OK) return fail(FB_ERR_CUDA, std::string("fast kernel launch failed: ") +
+                                               cudaGetErrorString(cudaGetLastError()));
+  if (done) g_launches += 2;
   if (!done) {
     const size_t s1 = generic::k1_smem<T>(W), s2 = generic::k2_smem<T>(W);
     dim3 g1((a.wpad + generic::K1_TC - 1) / generic::K1_TC, (band_rows + generic::K1_RB - 1) / generic::K1_RB);
     dim3 g2((j.cols + generic::K2_TW - 1) / generic::K2_TW, (band_rows + generic::K2_TH - 1) / generic::K2_TH);
-    if (j.kind == FB_BOX) {
-      FB_CUDA(cudaFuncSetAttribute(generic::k1_gen_vpass<T, kKindBox>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
-      FB_CUDA(cudaFuncSetAttribute(generic::k2_hpass_horner<T, kKindBox>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
-      generic::k1_gen_vpass<T, kKindBox><<<g1, generic::K1_TC * generic::K1_RG, s1, ctx->stream>>>(a);
-      FB_CUDA(cudaGetLastError());
-      generic::k2_hpass_horner<T, kKindBox><<<g2, 256, s2, ctx->stream>>>(a);
-      FB_CUDA(cudaGetLastError());
-    } else {
-      FB_CUDA(cudaFuncSetAttribute(generic::k1_gen_vpass<T, kKindGauss>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
-      FB_CUDA(cudaFuncSetAttribute(generic::k2_hpass_horner<T, kKindGauss>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
-      generic::k1_gen_vpass<T, kKindGauss><<<g1, generic::K1_TC * generic::K1_RG, s1, ctx->stream>>>(a);
-      FB_CUDA(cudaGetLastError());
-      generic::k2_hpass_horner<T, kKindGauss><<<g2, 256, s2, ctx->stream>>>(a);
-      FB_CUDA(cudaGetLastError());
-    }
+    auto k1 = j.kind == FB_BOX ? generic::k1_gen_vpass<T, kKindBox> : generic::k1_gen_vpass<T, kKindGauss>;
+    auto k2 = j.kind == FB_BOX ? generic::k2_hpass_horner<T, kKindBox> : generic::k2_hpass_horner<T, kKindGauss>;
+    FB_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
+    FB_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
+    FB_CUDA(cudaEventRecord(e0, ctx->stream));
+    k1<<<g1, generic::K1_TC * generic::K1_RG, s1, ctx->stream>>>(a);
+    FB_CUDA(cudaGetLastError());
+    FB_CUDA(cudaEventRecord(e1, ctx->stream));
+    k2<<<g2, 256, s2, ctx->stream>>>(a);
+    FB_CUDA(cudaGetLastError());
+    FB_CUDA(cudaEventRecord(e2, ctx->stream));
     g_launches += 2;
   }
   return FB_OK;
@@ -161,6 +176,32 @@ int run_job(fb_ctx* ctx, const Job& j, fb_stats* st) {
     a.norm = T(1);
     for (int k = 0; k < n_taps; ++k) a.w[k] = (T)j.taps[k];
   }
+  if (j.W <= kFastMaxW) {
+    for (int q = 0; q <= n_taps; ++q) {
+      a.wq[2 * q] = q < n_taps ? (float)a.w[q] : 0.f;
+      a.wq[2 * q + 1] = q > 0 ? (float)a.w[q - 1] : 0.f;
+    }
+  }
+  // channel constants 1/sqrt(m), sqrt(m) (rounded once from double)
+  if (j.N + 1 > ctx->tab_cap) {
+    if (ctx->tab) cudaFree(ctx->tab);
+    if (ctx->tab_host) cudaFreeHost(ctx->tab_host);
+    ctx->tab = nullptr;
+    ctx->tab_host = nullptr;
+    ctx->tab_cap = 0;
+    const int cap = std::max(j.N + 1, 256);
+    FB_CUDA(cudaMalloc(&ctx->tab, 2 * sizeof(float) * cap));
+    FB_CUDA(cudaMallocHost(&ctx->tab_host, 2 * sizeof(float) * cap));
+    ctx->tab_cap = cap;
+  }
+  FB_CUDA(cudaStreamSynchronize(ctx->stream));  // the pinned staging may still feed an earlier copy
+  for (int m = 0; m <= j.N; ++m) {
+    ctx->tab_host[2 * m] = m > 0 ? (float)(1.0 / std::sqrt((double)m)) : 0.f;
+    ctx->tab_host[2 * m + 1] = (float)std::sqrt((double)m);
+  }
+  FB_CUDA(cudaMemcpyAsync(ctx->tab, ctx->tab_host, 2 * sizeof(float) * (j.N + 1), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  a.tab = ctx->tab;
   a.wpad = j.cols + 2 * j.W;
   a.pitch = (a.wpad + 31) / 32 * 32;
 
@@ -233,6 +274,7 @@ int execute(fb_ctx* ctx, const fb_image* in, int halo_top, int halo_bottom, fb_i
 
   FB_CUDA(cudaMemcpyAsync(ctx->flags, ctx->flags_host, 4 * sizeof(unsigned long long), cudaMemcpyHostToDevice,
                           ctx->stream));
+  ctx->kev_used = 0;
   const long long launches0 = g_launches.load();
   FB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
   if (out) {
@@ -291,6 +333,13 @@ int execute(fb_ctx* ctx, const fb_image* in, int halo_top, int halo_bottom, fb_i
   cudaEventElapsedTime(&kms, ctx->ev[1], ctx->ev[2]);
   local.device_ms = ms;
   local.kernel_ms = kms;
+  for (int b = 0; b + 2 < ctx->kev_used; b += 3) {
+    float t1 = 0.f, t2 = 0.f;
+    cudaEventElapsedTime(&t1, ctx->kev[b], ctx->kev[b + 1]);
+    cudaEventElapsedTime(&t2, ctx->kev[b + 1], ctx->kev[b + 2]);
+    local.k1_ms += t1;
+    local.k2_ms += t2;
+  }
   local.spatial_filter_calls = j.N + 1;
   local.order = j.mode == kModeGpa ? j.N : 0;
   if (st) *st = local;
@@ -342,8 +391,11 @@ int fb_destroy(fb_ctx* c) {
   if (c->out_stage) cudaFree(c->out_stage);
   if (c->flags) cudaFree(c->flags);
   if (c->flags_host) cudaFreeHost(c->flags_host);
+  if (c->tab) cudaFree(c->tab);
+  if (c->tab_host) cudaFreeHost(c->tab_host);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : c->kev) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->own_stream);
   delete c;
   return FB_OK;

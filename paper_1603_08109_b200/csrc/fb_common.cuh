@@ -17,6 +17,7 @@ namespace fbgpu {
 
 constexpr int kMaxW = 160;                  // largest half-width the kernels accept
 constexpr int kMaxTaps = 2 * kMaxW + 1;
+constexpr int kFastMaxW = 32;               // largest half-width of the specialised fp32 kernels
 
 enum : int { kModeGpa = 0, kModePlain = 1 };
 enum : int { kKindBox = 0, kKindGauss = 1 };
@@ -54,7 +55,11 @@ struct GpaArgs {
   long long out_ld;
   int out_dtype;      // 1 f32, 2 f64
   unsigned long long* flags;
+  const float* tab;   // fp32 channel constants: tab[2m] = 1/sqrt(m) (0 for m = 0), tab[2m+1] = sqrt(m)
   T w[kMaxTaps];      // normalised 1-D taps (gaussian)
+  // Tap pairs for packed FFMA2 (fp32 fast path): wq[2a] = w[a], wq[2a+1] = w[a-1],
+  // a = 0 .. 2W+1, with w[-1] = w[2W+1] = 0 (box: all ones).
+  alignas(8) float wq[2 * (2 * kFastMaxW + 2)];
 };
 
 __device__ __forceinline__ double load_sample(const void* f, int dt, long long idx) {

