@@ -182,6 +182,8 @@ int run_job(fb_ctx* ctx, const Job& j, fb_stats* st) {
       a.wq[2 * q + 1] = q > 0 ? (float)a.w[q - 1] : 0.f;
     }
   }
+  for (int m = 0; m < kWalkMaxCh; ++m)
+    a.rsc2[2 * m] = a.rsc2[2 * m + 1] = m > 0 ? (float)(1.0 / std::sqrt((double)m)) : 0.f;
   // channel constants 1/sqrt(m), sqrt(m) (rounded once from double)
   if (j.N + 1 > ctx->tab_cap) {
     if (ctx->tab) cudaFree(ctx->tab);
@@ -212,8 +214,9 @@ int run_job(fb_ctx* ctx, const Job& j, fb_stats* st) {
   if (band < 64) band = 64;
   const long long rows_pad = (j.rows_out + 63) / 64 * 64;
   if (band > rows_pad) band = rows_pad;
-  a.plane = band * a.pitch;
-  int rc = grow(&ctx->ws, &ctx->ws_bytes, (size_t)(j.N + 1) * a.plane * sizeof(T));
+  a.rstride = (long long)(j.N + 1) * a.pitch;
+  a.band_max = (int)band;
+  int rc = grow(&ctx->ws, &ctx->ws_bytes, (size_t)band * a.rstride * sizeof(T));
   if (rc != FB_OK) return rc;
   a.v = reinterpret_cast<T*>(ctx->ws);
 

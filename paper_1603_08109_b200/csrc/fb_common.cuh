@@ -3,11 +3,14 @@
 // Data layout in HBM:
 //   input f      : row-major, leading dim f_ld, dtype u8/f32/f64, rows_in rows
 //                  (rows [halo_top, rows_in - halo_bottom) are the rows to filter)
-//   channel planes v : T[N+1][band_rows_max][pitch], pitch = round_up(cols + 2W, 32).
-//                  Plane n holds the VERTICALLY filtered channel c_n = e x^n / sqrt(n!)
-//                  of the current row band, with W replicate columns on each side
-//                  (padded column pc <-> image column clamp(pc - W, 0, cols-1)),
-//                  so the horizontal pass never leaves the plane.
+//   channel planes v : T[band_rows_max][N+1][pitch] (row-interleaved), pitch = round_up(cols + 2W, 32).
+//                  v[(o * (N+1) + n) * pitch + pc] is the VERTICALLY filtered channel
+//                  c_n = e x^n / sqrt(n!) at band row o and padded column pc, with W
+//                  replicate columns on each side (pc <-> image column clamp(pc - W, 0, cols-1)),
+//                  so the horizontal pass never leaves the row.  Interleaving the channels
+//                  of a row puts all N+1 stores of one output row within a few MB of each
+//                  other (immediate-offset stores); kernel 2 fetches per-channel tiles with
+//                  a 3-D TMA map {pitch, N+1, rows}.
 //   output       : row-major f32/f64, leading dim out_ld.
 #pragma once
 #include <cuda_runtime.h>
@@ -37,9 +40,10 @@ struct GpaArgs {
   int band_rows;      // output rows in the band
   // channel planes (workspace)
   T* v;
-  long long pitch;    // elements per plane row
-  long long plane;    // elements per plane
+  long long pitch;    // elements per plane row (= distance between channels of one row)
+  long long rstride;  // elements between consecutive rows of one channel = (N+1) * pitch
   int wpad;           // cols + 2W  (valid padded columns)
+  int band_max;       // rows the workspace holds
   // filter
   int W;
   int N;
@@ -60,7 +64,12 @@ struct GpaArgs {
   // Tap pairs for packed FFMA2 (fp32 fast path): wq[2a] = w[a], wq[2a+1] = w[a-1],
   // a = 0 .. 2W+1, with w[-1] = w[2W+1] = 0 (box: all ones).
   alignas(8) float wq[2 * (2 * kFastMaxW + 2)];
+  // (1/sqrt(n), 1/sqrt(n)) pairs for n < kWalkMaxCh, compile-time-indexed by the box walker
+  alignas(8) float rsc2[2 * 64];
+  int walk_rows;      // output rows per thread of the box walker
 };
+
+constexpr int kWalkMaxCh = 64;              // channels (N+1) the register-resident box walker holds
 
 __device__ __forceinline__ double load_sample(const void* f, int dt, long long idx) {
   if (dt == 1) return (double)__ldg(reinterpret_cast<const float*>(f) + idx);

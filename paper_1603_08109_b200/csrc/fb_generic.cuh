@@ -81,14 +81,14 @@ __global__ void __launch_bounds__(K1_TC * K1_RG) k1_gen_vpass(const GpaArgs<T> a
       for (int i = g; i < TR; i += K1_RG) cs[i * K1_TC + tc] = cs[i * K1_TC + tc] * (xs[i * K1_TC + tc] * rs);
     }
     __syncthreads();
-    T* vp = a.v + (long long)n * a.plane;
+    T* vp = a.v + (long long)n * a.pitch;
     const bool col_ok = pc < a.wpad;
     if (KIND == kKindBox) {
       T s = T(0);
       for (int k = 0; k <= 2 * W; ++k) s += cs[(ob + k) * K1_TC + tc];
       for (int r = 0; r < K1_R; ++r) {
         const int o = o0 + ob + r;
-        if (col_ok && o < a.band_rows) vp[(long long)o * a.pitch + pc] = s;
+        if (col_ok && o < a.band_rows) vp[(long long)o * a.rstride + pc] = s;
         s += cs[(ob + r + 2 * W + 1) * K1_TC + tc] - cs[(ob + r) * K1_TC + tc];
       }
     } else {
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(K1_TC * K1_RG) k1_gen_vpass(const GpaArgs<T> a
         T acc = T(0);
         for (int k = 0; k <= 2 * W; ++k) acc = fma(a.w[k], cs[(ob + r + k) * K1_TC + tc], acc);
         const int o = o0 + ob + r;
-        if (col_ok && o < a.band_rows) vp[(long long)o * a.pitch + pc] = acc;
+        if (col_ok && o < a.band_rows) vp[(long long)o * a.rstride + pc] = acc;
       }
     }
     __syncthreads();
@@ -131,11 +131,11 @@ __global__ void __launch_bounds__(256) k2_hpass_horner(const GpaArgs<T> a) {
 
   T rs_next = T(0);  // 1/sqrt(m+1) of the previous (higher) channel
   for (int m = a.N; m >= 0; --m) {
-    const T* vp = a.v + (long long)m * a.plane;
+    const T* vp = a.v + (long long)m * a.pitch;
     for (int idx = threadIdx.x; idx < K2_TH * LW; idx += blockDim.x) {
       const int rr = idx / LW, cc = idx - rr * LW;
       const int gr = y0 + rr, gc = x0 + cc;
-      tile[idx] = (gr < a.band_rows && gc < a.wpad) ? vp[(long long)gr * a.pitch + gc] : T(0);
+      tile[idx] = (gr < a.band_rows && gc < a.wpad) ? vp[(long long)gr * a.rstride + gc] : T(0);
     }
     __syncthreads();
     const T* row = tile + r * LW + c0;
