@@ -136,15 +136,19 @@ def algorithmic_flops(cfg, N):
     return {"k1": (N + 1) * (per_pass + 2), "k2": (N + 1) * (per_pass + 6)}
 
 
-def ncu_traffic(config, kernel):
-    """dram bytes per launch for `kernel` from the committed ncu summary of this config, else None."""
+def ncu_traffic(config, stage):
+    """(kernel name, dram bytes per launch) of pipeline stage 'k1'/'k2' from the committed ncu
+    summary of this config (profiles/ncu_<config>.json, tools/ncu_summary.py), else (None, None)."""
     path = os.path.join(ROOT, "profiles", f"ncu_{config}.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return d["kernels"][kernel]["dram_bytes_per_launch"]
+        for name, k in d["kernels"].items():
+            if name.startswith(stage):
+                return name, k["dram_bytes_per_launch"], d.get("pixels_per_launch")
     except Exception:
-        return None
+        pass
+    return None, None, None
 
 
 # ----------------------------------------------------------------------------- reference arm (CPU)
@@ -243,7 +247,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_1603_08109_b200 import _native, gpa_filter, sharding
+    from paper_1603_08109_b200 import _native, gpa_filter, gpa_filter_batch, sharding
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -290,9 +294,12 @@ def main():
                              halo_top=top, halo_bottom=bottom)
             sts = [st]
             sharding.gather_rows(dev_out[0], root_full, rank, world, bands)
+        elif len(dev_imgs) > 1:
+            sts = [_native.gpa_batch(dev_imgs, dev_out, kernel, cfg.sigma_r, N, 128.0, 128.0,
+                                     _native.FB_PREC_F32, local)]
         else:
-            sts = [_native.gpa(im, o, kernel, cfg.sigma_r, N, 128.0, 128.0, _native.FB_PREC_F32, local)
-                   for im, o in zip(dev_imgs, dev_out)]
+            sts = [_native.gpa(dev_imgs[0], dev_out[0], kernel, cfg.sigma_r, N, 128.0, 128.0,
+                               _native.FB_PREC_F32, local)]
         if record:
             for st in sts:
                 kstats["k1_ms"] += st["k1_ms"]
@@ -338,8 +345,10 @@ def main():
         pinned_out = [torch.empty(im.shape, dtype=torch.float64).pin_memory().numpy() for im in host_imgs]
 
         def e2e_step():
-            for im, o in zip(pinned_in, pinned_out):
-                gpa_filter(im, kernel, cfg.sigma_r, N, precision="f32", device=local, out=o)
+            if len(pinned_in) > 1:
+                gpa_filter_batch(pinned_in, kernel, cfg.sigma_r, N, precision="f32", device=local, outs=pinned_out)
+            else:
+                gpa_filter(pinned_in[0], kernel, cfg.sigma_r, N, precision="f32", device=local, out=pinned_out[0])
 
         e2e_step()
         if world > 1:
@@ -357,9 +366,11 @@ def main():
         e2e = {"value": total_px * n_e2e / (float(t_t.item()) * 1e-3) / 1e6, "unit": "MP/s",
                "h2d_bytes_per_step": int(sum(im.nbytes for im in pinned_in)) * world,
                "d2h_bytes_per_step": int(sum(o.nbytes for o in pinned_out)) * world,
-               "path": "gpa_filter(numpy pinned f32 in, out=pinned f64) per image/band; bands with halos are "
-                       "filtered per rank without exchange in this leg" if bands is not None else
-                       "gpa_filter(numpy pinned f32 in, out=pinned f64)"}
+               "path": ("gpa_filter_batch" if len(pinned_in) > 1 else "gpa_filter")
+               + "(pinned float32 numpy in, out= pinned float64 numpy): H2D, kernels and D2H pipelined on "
+                 "three streams inside the call"
+               + ("; at N>1 each rank filters its own band (halo rows replicated at band edges in this leg)"
+                  if bands is not None else "")}
 
     if rank != 0:
         if world > 1:
@@ -390,14 +401,19 @@ def main():
     dom = max(("k1", "k2"), key=lambda n: kstats[f"{n}_ms"])
     dk = kernels[dom]
     bound = "hbm" if dk["hbm_frac"] >= dk["fp32_frac"] else "fp32"
-    kname = {"k1": "k1_gen_vpass", "k2": "k2_hpass_horner"}[dom]
+    kname, traffic, traffic_px = ncu_traffic(cfg.name, dom)
+    px_per_launch = my_pixels * args.steps / launches_per_kernel
+    if traffic is not None and traffic_px and abs(traffic_px - px_per_launch) > 1:
+        traffic = traffic * px_per_launch / traffic_px  # profile captured on a different launch size
     roofline = {
-        "bound": bound, "kernel": kname,
+        "bound": bound, "kernel": kname or dom,
         "achieved": dk["hbm_gbs"] if bound == "hbm" else dk["fp32_tflops"],
         "peak": hbm_peak if bound == "hbm" else FP32_NOMINAL_TFLOPS,
         "unit": "GB/s" if bound == "hbm" else "TFLOP/s",
         "frac": dk["hbm_frac"] if bound == "hbm" else dk["fp32_frac"],
-        "traffic": ncu_traffic(cfg.name, kname),
+        "traffic": traffic,
+        "traffic_source": "profiles/ncu_%s.json (ncu --set full, dram__bytes_read+write per launch)" % cfg.name
+        if traffic is not None else None,
         "peak_source": peak_src if bound == "hbm" else "nominal 148 SM x 128 FMA/clk x 1.965 GHz",
         "alg_bytes_per_px": dk["alg_bytes_per_px"],
         "pipeline_hbm_frac": bpp["pipeline"] * total_px * args.steps / (ms_max * 1e-3) / 1e9 / hbm_peak,

@@ -92,6 +92,7 @@ typedef struct fb_stats {
   int32_t bands;                /* row bands the workspace limit split the image into */
   int32_t precision;            /* fb_precision actually used */
   int64_t launches;             /* kernels launched by this call */
+  int64_t bad_image;            /* batch index of the image bad_index refers to (-1: none) */
 } fb_stats;
 
 /* Context lifecycle (the reference is stateless; the context is where the
@@ -114,6 +115,9 @@ int fb_set_workspace_limit(fb_ctx* ctx, int64_t bytes);
  * buffer are replicated from its first/last row (the reference's edge pad).
  * Only the output rows are checked for finiteness / range [center -
  * half_range, center + half_range] (image.py:35-54).
+ * Host-resident images of more than 4 MP are processed in 8 row chunks whose
+ * copy-in, kernels and copy-out overlap on three streams (pinned host memory
+ * makes the copies asynchronous; pageable memory still works, serialised).
  * `out` must be FB_F32 or FB_F64 (the reference returns float64).
  * The caller validates sigma_r and the order (engine.py:40-49) and the box
  * window (conv.py:19-27); they are re-checked here and reported as FB_ERR_PARAM.
@@ -121,6 +125,17 @@ int fb_set_workspace_limit(fb_ctx* ctx, int64_t bytes);
 int fb_gpa_filter(fb_ctx* ctx, const fb_image* in, int64_t halo_top, int64_t halo_bottom,
                   fb_image* out, const fb_spatial* spatial, double sigma_r, int32_t order,
                   double center, double half_range, int32_t precision, fb_stats* stats);
+
+/*
+ * fb_gpa_filter_batch — the by-image partitioning of a batch (config c3):
+ * `count` images of equal width, each filtered exactly as fb_gpa_filter
+ * (no halos).  Host-resident images are pipelined: the copy-in of image i+1
+ * and the copy-out of image i-1 overlap the kernels of image i (three CUDA
+ * streams).  On an input error stats->bad_image names the offending image.
+ */
+int fb_gpa_filter_batch(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int32_t count,
+                        const fb_spatial* spatial, double sigma_r, int32_t order, double center,
+                        double half_range, int32_t precision, fb_stats* stats);
 
 /*
  * fb_spatial_filter — replaces apply_spatial / box_filter / gaussian_filter

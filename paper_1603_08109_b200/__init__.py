@@ -10,7 +10,7 @@ no CPU fallback.
 """
 
 from .conv import apply_spatial, box_filter, gaussian_filter
-from .engine import gpa_filter, gpa_filter_auto
+from .engine import gpa_filter, gpa_filter_auto, gpa_filter_batch
 from .errors import (BoundInapplicableError, NativeError, NumericRangeError, ParameterError,
                      RangeViolationError)
 from .image import RANGE_8BIT, RangeSpec, as_image, center, uncenter, validate_range
@@ -24,6 +24,7 @@ __all__ = [
     "OrderEstimate", "RangeSpec", "SpatialKernel", "RANGE_8BIT", "__version__",
     "apply_spatial", "as_image", "box_filter", "center", "chernoff_order_exhaustive",
     "epsilon_from_delta", "estimate_order", "gaussian_filter", "gpa_filter", "gpa_filter_auto",
+    "gpa_filter_batch",
     "lambert_w0_series", "log_chernoff", "make_spatial_kernel", "uncenter", "validate_range",
     "BoundInapplicableError", "NativeError", "NumericRangeError", "ParameterError",
     "RangeViolationError",

@@ -28,7 +28,8 @@ FB_PREC_F32, FB_PREC_F64 = 1, 2
 #: Every symbol include/fbgpu.h declares (checked by tests/test_native_abi.py).
 EXPORTED_SYMBOLS = (
     "fb_create", "fb_destroy", "fb_set_stream", "fb_set_workspace_limit", "fb_gpa_filter",
-    "fb_spatial_filter", "fb_validate", "fb_last_error", "fb_version", "fb_launch_count",
+    "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate", "fb_last_error", "fb_version",
+    "fb_launch_count",
 )
 
 
@@ -49,7 +50,8 @@ class FbStats(ctypes.Structure):
                 ("device_ms", ctypes.c_double), ("kernel_ms", ctypes.c_double),
                 ("k1_ms", ctypes.c_double), ("k2_ms", ctypes.c_double),
                 ("h2d_bytes", ctypes.c_int64), ("d2h_bytes", ctypes.c_int64),
-                ("bands", ctypes.c_int32), ("precision", ctypes.c_int32), ("launches", ctypes.c_int64)]
+                ("bands", ctypes.c_int32), ("precision", ctypes.c_int32), ("launches", ctypes.c_int64),
+                ("bad_image", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {name: getattr(self, name) for name, _ in self._fields_}
@@ -79,13 +81,16 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         lib.fb_gpa_filter.argtypes = [vp, P(FbImage), ctypes.c_int64, ctypes.c_int64, P(FbImage), P(FbSpatial),
                                       ctypes.c_double, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
                                       ctypes.c_int32, P(FbStats)]
+        lib.fb_gpa_filter_batch.argtypes = [vp, P(FbImage), P(FbImage), ctypes.c_int32, P(FbSpatial),
+                                            ctypes.c_double, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                            ctypes.c_int32, P(FbStats)]
         lib.fb_spatial_filter.argtypes = [vp, P(FbImage), P(FbImage), P(FbSpatial), ctypes.c_int32, P(FbStats)]
         lib.fb_validate.argtypes = [vp, P(FbImage), ctypes.c_double, ctypes.c_double, P(FbStats)]
         lib.fb_last_error.restype = ctypes.c_char_p
         lib.fb_version.restype = ctypes.c_int
         lib.fb_launch_count.restype = ctypes.c_int64
         for name in ("fb_create", "fb_destroy", "fb_set_stream", "fb_set_workspace_limit", "fb_gpa_filter",
-                     "fb_spatial_filter", "fb_validate"):
+                     "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
         return lib
@@ -185,6 +190,24 @@ def gpa(src, out, kernel, sigma_r: float, order: int, center: float, half_range:
                            ctypes.byref(sp), float(sigma_r), int(order), float(center), float(half_range),
                            int(precision), ctypes.byref(st))
     _check(lib, rc, src, st, center - half_range, center + half_range)
+    return st.as_dict()
+
+
+def gpa_batch(srcs, outs, kernel, sigma_r: float, order: int, center: float, half_range: float,
+              precision: int, device: int = 0) -> dict:
+    """Run fb_gpa_filter_batch over equally wide images (numpy arrays or CUDA tensors)."""
+    lib = load_library()
+    ctx = context(device)
+    lib.fb_set_stream(ctx, _stream_for(srcs[0], device))
+    sp, _taps = spatial_desc(kernel)
+    n = len(srcs)
+    ins = (FbImage * n)(*[image_desc(s) for s in srcs])
+    outs_d = (FbImage * n)(*[image_desc(o) for o in outs])
+    st = FbStats()
+    rc = lib.fb_gpa_filter_batch(ctx, ins, outs_d, n, ctypes.byref(sp), float(sigma_r), int(order),
+                                 float(center), float(half_range), int(precision), ctypes.byref(st))
+    bad = srcs[st.bad_image] if st.bad_image >= 0 else srcs[0]
+    _check(lib, rc, bad, st, center - half_range, center + half_range)
     return st.as_dict()
 
 

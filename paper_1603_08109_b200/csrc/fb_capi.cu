@@ -41,33 +41,43 @@ size_t dtype_size(int dt) { return dt == FB_U8 ? 1 : (dt == FB_F32 ? 4 : 8); }
 
 struct fb_ctx {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // compute stream (the caller's, or own_stream)
   cudaStream_t own_stream = nullptr;
-  void* ws = nullptr;
+  cudaStream_t s_h2d = nullptr;       // host -> device copies of the pipelined host path
+  cudaStream_t s_d2h = nullptr;       // device -> host copies
+  void* ws = nullptr;                 // channel planes of one row band
   size_t ws_bytes = 0;
-  void* in_stage = nullptr;
-  size_t in_stage_bytes = 0;
-  void* out_stage = nullptr;
-  size_t out_stage_bytes = 0;
-  unsigned long long* flags = nullptr;       // device, 4 slots
+  void* in_stage[2] = {nullptr, nullptr};   // device copies of host inputs (double-buffered per image)
+  size_t in_stage_bytes[2] = {0, 0};
+  void* out_stage[2] = {nullptr, nullptr};  // device outputs bound for host memory
+  size_t out_stage_bytes[2] = {0, 0};
+  unsigned long long* flags = nullptr;       // device, 4 slots per image of a batch
+  unsigned long long* flags_host = nullptr;  // pinned readback
+  int flags_cap = 0;                         // images the flag buffers hold
   float* tab = nullptr;                      // device channel-constant table (fp32 fast path)
   float* tab_host = nullptr;                 // pinned staging for it
+  double* tabd = nullptr;                    // matching fp64 Horner constants
+  double* tabd_host = nullptr;
   int tab_cap = 0;                           // channels it holds
-  unsigned long long* flags_host = nullptr;  // pinned, 8 slots (0-3 init pattern, 4-7 readback)
+  int tab_n = -1;                            // order N the table currently holds
   long long ws_limit = 0;
   int sm_count = 148;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_start = nullptr, ev_kstart = nullptr, ev_kend = nullptr, ev_end = nullptr;
   // Per-band kernel boundaries: [k1 start, k1 end = k2 start, k2 end] x bands.
   std::vector<cudaEvent_t> kev;
   int kev_used = 0;
+  std::vector<cudaEvent_t> pev;  // pipeline events (copy/compute hand-offs)
+  int pev_used = 0;
 
-  cudaEvent_t next_event() {
-    if (kev_used == (int)kev.size()) {
+  cudaEvent_t next_kev() { return take(kev, kev_used, cudaEventDefault); }
+  cudaEvent_t next_pev() { return take(pev, pev_used, cudaEventDisableTiming); }
+  static cudaEvent_t take(std::vector<cudaEvent_t>& pool, int& used, unsigned flags) {
+    if (used == (int)pool.size()) {
       cudaEvent_t e = nullptr;
-      cudaEventCreate(&e);
-      kev.push_back(e);
+      cudaEventCreateWithFlags(&e, flags);
+      pool.push_back(e);
     }
-    return kev[kev_used++];
+    return pool[used++];
   }
 };
 
@@ -99,62 +109,17 @@ int check_image(const fb_image* im, const char* what, bool allow_u8) {
   return FB_OK;
 }
 
-// Everything one filter call needs, independent of precision.
+// Filter parameters shared by every image of a call, independent of precision.
 struct Job {
-  const void* f;       // device input
-  long long f_ld;
-  int f_dtype;
-  int rows_in, cols, halo_top, rows_out;
-  void* out;           // device output
-  long long out_ld;
-  int out_dtype;
   int kind, W, N, mode, check;
   const double* taps;
   double sr, tc, lo, hi;
 };
 
+// The precision-typed argument block: constants once per call, pointers per image.
 template <typename T>
-int launch_band(fb_ctx* ctx, const Job& j, GpaArgs<T>& a, int band_row0, int band_rows) {
-  a.band_row0 = band_row0;
-  a.band_rows = band_rows;
-  const int W = j.W;
-  bool done = false;
-  cudaEvent_t e0 = ctx->next_event(), e1 = ctx->next_event(), e2 = ctx->next_event();
-  KernelEvents kev{e0, e1, e2};
-  int rc = launch_fast<T>(ctx->stream, j.kind, W, a, kev, &done);
-  if (rc != FB_OK) return fail(FB_ERR_CUDA, std::string("fast kernel launch failed: ") +
-                                               cudaGetErrorString(cudaGetLastError()));
-  if (done) g_launches += 2;
-  if (!done) {
-    const size_t s1 = generic::k1_smem<T>(W), s2 = generic::k2_smem<T>(W);
-    dim3 g1((a.wpad + generic::K1_TC - 1) / generic::K1_TC, (band_rows + generic::K1_RB - 1) / generic::K1_RB);
-    dim3 g2((j.cols + generic::K2_TW - 1) / generic::K2_TW, (band_rows + generic::K2_TH - 1) / generic::K2_TH);
-    auto k1 = j.kind == FB_BOX ? generic::k1_gen_vpass<T, kKindBox> : generic::k1_gen_vpass<T, kKindGauss>;
-    auto k2 = j.kind == FB_BOX ? generic::k2_hpass_horner<T, kKindBox> : generic::k2_hpass_horner<T, kKindGauss>;
-    FB_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
-    FB_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
-    FB_CUDA(cudaEventRecord(e0, ctx->stream));
-    k1<<<g1, generic::K1_TC * generic::K1_RG, s1, ctx->stream>>>(a);
-    FB_CUDA(cudaGetLastError());
-    FB_CUDA(cudaEventRecord(e1, ctx->stream));
-    k2<<<g2, 256, s2, ctx->stream>>>(a);
-    FB_CUDA(cudaGetLastError());
-    FB_CUDA(cudaEventRecord(e2, ctx->stream));
-    g_launches += 2;
-  }
-  return FB_OK;
-}
-
-template <typename T>
-int run_job(fb_ctx* ctx, const Job& j, fb_stats* st) {
-  GpaArgs<T> a;
+int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a, int* band_out) {
   memset(&a, 0, sizeof(a));
-  a.f = j.f;
-  a.f_ld = j.f_ld;
-  a.f_dtype = j.f_dtype;
-  a.rows_in = j.rows_in;
-  a.cols = j.cols;
-  a.halo_top = j.halo_top;
   a.W = j.W;
   a.N = j.N;
   a.mode = j.mode;
@@ -164,10 +129,7 @@ int run_job(fb_ctx* ctx, const Job& j, fb_stats* st) {
   a.inv_sr = j.mode == kModeGpa ? 1.0 / j.sr : 0.0;
   a.lo = j.lo;
   a.hi = j.hi;
-  a.out = j.out;
-  a.out_ld = j.out_ld;
-  a.out_dtype = j.out_dtype;
-  a.flags = ctx->flags;
+  a.cols = cols;
   const int n_taps = 2 * j.W + 1;
   if (j.kind == FB_BOX) {
     a.norm = (T)(1.0 / ((double)n_taps * n_taps));
@@ -184,156 +146,339 @@ int run_job(fb_ctx* ctx, const Job& j, fb_stats* st) {
   }
   for (int m = 0; m < kWalkMaxCh; ++m)
     a.rsc2[2 * m] = a.rsc2[2 * m + 1] = m > 0 ? (float)(1.0 / std::sqrt((double)m)) : 0.f;
-  // channel constants 1/sqrt(m), sqrt(m) (rounded once from double)
+  // channel constants 1/sqrt(m), sqrt(m) (rounded once from double), uploaded when N changes
   if (j.N + 1 > ctx->tab_cap) {
-    if (ctx->tab) cudaFree(ctx->tab);
-    if (ctx->tab_host) cudaFreeHost(ctx->tab_host);
+    for (void* p : {(void*)ctx->tab, (void*)ctx->tabd}) if (p) cudaFree(p);
+    for (void* p : {(void*)ctx->tab_host, (void*)ctx->tabd_host}) if (p) cudaFreeHost(p);
     ctx->tab = nullptr;
     ctx->tab_host = nullptr;
+    ctx->tabd = nullptr;
+    ctx->tabd_host = nullptr;
     ctx->tab_cap = 0;
+    ctx->tab_n = -1;
     const int cap = std::max(j.N + 1, 256);
-    FB_CUDA(cudaMalloc(&ctx->tab, 2 * sizeof(float) * cap));
-    FB_CUDA(cudaMallocHost(&ctx->tab_host, 2 * sizeof(float) * cap));
+    FB_CUDA(cudaMalloc(&ctx->tab, 4 * sizeof(float) * cap));
+    FB_CUDA(cudaMallocHost(&ctx->tab_host, 4 * sizeof(float) * cap));
+    FB_CUDA(cudaMalloc(&ctx->tabd, 2 * sizeof(double) * cap));
+    FB_CUDA(cudaMallocHost(&ctx->tabd_host, 2 * sizeof(double) * cap));
     ctx->tab_cap = cap;
   }
-  FB_CUDA(cudaStreamSynchronize(ctx->stream));  // the pinned staging may still feed an earlier copy
-  for (int m = 0; m <= j.N; ++m) {
-    ctx->tab_host[2 * m] = m > 0 ? (float)(1.0 / std::sqrt((double)m)) : 0.f;
-    ctx->tab_host[2 * m + 1] = (float)std::sqrt((double)m);
+  if (ctx->tab_n != j.N) {
+    FB_CUDA(cudaStreamSynchronize(ctx->stream));  // the pinned staging may still feed an earlier copy
+    for (int m = 0; m <= j.N; ++m) {
+      // r_m: the fp32 constant kernel 1 multiplies channel m by.  The fp64 Horner constants are
+      // derived from r_m itself so the normalisation cancels exactly (no 1/sqrt(n!) drift).
+      const float r = m > 0 ? (float)(1.0 / std::sqrt((double)m)) : 0.f;
+      const double h = m > 0 ? 1.0 / ((double)m * (double)r) : 0.0;
+      const double sg = m > 0 ? 1.0 / (double)r : 0.0;
+      ctx->tab_host[4 * m] = r;
+      ctx->tab_host[4 * m + 1] = (float)std::sqrt((double)m);
+      ctx->tab_host[4 * m + 2] = (float)h;
+      ctx->tab_host[4 * m + 3] = (float)sg;
+      ctx->tabd_host[2 * m] = h;
+      ctx->tabd_host[2 * m + 1] = sg;
+    }
+    FB_CUDA(cudaMemcpyAsync(ctx->tab, ctx->tab_host, 4 * sizeof(float) * (j.N + 1), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    FB_CUDA(cudaMemcpyAsync(ctx->tabd, ctx->tabd_host, 2 * sizeof(double) * (j.N + 1), cudaMemcpyHostToDevice,
+                            ctx->stream));
+    ctx->tab_n = j.N;
   }
-  FB_CUDA(cudaMemcpyAsync(ctx->tab, ctx->tab_host, 2 * sizeof(float) * (j.N + 1), cudaMemcpyHostToDevice,
-                          ctx->stream));
   a.tab = ctx->tab;
-  a.wpad = j.cols + 2 * j.W;
+  a.tabd = ctx->tabd;
+  a.wpad = cols + 2 * j.W;
   a.pitch = (a.wpad + 31) / 32 * 32;
-
   // Row bands: the N+1 planes of one band must fit under the workspace limit.
   const long long per_row = (long long)(j.N + 1) * a.pitch * (long long)sizeof(T);
   long long band = ctx->ws_limit / std::max(per_row, 1ll);
   band = band / 64 * 64;
   if (band < 64) band = 64;
-  const long long rows_pad = (j.rows_out + 63) / 64 * 64;
+  const long long rows_pad = (rows_out_max + 63) / 64 * 64;
   if (band > rows_pad) band = rows_pad;
   a.rstride = (long long)(j.N + 1) * a.pitch;
   a.band_max = (int)band;
   int rc = grow(&ctx->ws, &ctx->ws_bytes, (size_t)band * a.rstride * sizeof(T));
   if (rc != FB_OK) return rc;
   a.v = reinterpret_cast<T*>(ctx->ws);
-
-  int bands = 0;
-  for (long long r0 = 0; r0 < j.rows_out; r0 += band) {
-    const int rows = (int)std::min<long long>(band, j.rows_out - r0);
-    rc = launch_band<T>(ctx, j, a, (int)r0, rows);
-    if (rc != FB_OK) return rc;
-    ++bands;
-  }
-  if (st) st->bands = bands;
+  *band_out = (int)band;
   return FB_OK;
 }
 
-// Copy-in / filter / copy-out around run_job, with flag readback and error mapping.
-int execute(fb_ctx* ctx, const fb_image* in, int halo_top, int halo_bottom, fb_image* out, Job j,
-            int precision, fb_stats* st) {
+template <typename T>
+int launch_band(fb_ctx* ctx, int kind, GpaArgs<T>& a, int band_row0, int band_rows) {
+  a.band_row0 = band_row0;
+  a.band_rows = band_rows;
+  const int W = a.W;
+  bool done = false;
+  cudaEvent_t e0 = ctx->next_kev(), e1 = ctx->next_kev(), e2 = ctx->next_kev();
+  KernelEvents kev{e0, e1, e2};
+  int rc = launch_fast<T>(ctx->stream, kind, W, a, kev, &done);
+  if (rc != FB_OK) return fail(FB_ERR_CUDA, std::string("fast kernel launch failed: ") +
+                                               cudaGetErrorString(cudaGetLastError()));
+  if (done) {
+    g_launches += 2;
+    return FB_OK;
+  }
+  const size_t s1 = generic::k1_smem<T>(W), s2 = generic::k2_smem<T>(W);
+  dim3 g1((a.wpad + generic::K1_TC - 1) / generic::K1_TC, (band_rows + generic::K1_RB - 1) / generic::K1_RB);
+  dim3 g2((a.cols + generic::K2_TW - 1) / generic::K2_TW, (band_rows + generic::K2_TH - 1) / generic::K2_TH);
+  auto k1 = kind == FB_BOX ? generic::k1_gen_vpass<T, kKindBox> : generic::k1_gen_vpass<T, kKindGauss>;
+  auto k2 = kind == FB_BOX ? generic::k2_hpass_horner<T, kKindBox> : generic::k2_hpass_horner<T, kKindGauss>;
+  FB_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
+  FB_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
+  FB_CUDA(cudaEventRecord(e0, ctx->stream));
+  k1<<<g1, generic::K1_TC * generic::K1_RG, s1, ctx->stream>>>(a);
+  FB_CUDA(cudaGetLastError());
+  FB_CUDA(cudaEventRecord(e1, ctx->stream));
+  k2<<<g2, 256, s2, ctx->stream>>>(a);
+  FB_CUDA(cudaGetLastError());
+  FB_CUDA(cudaEventRecord(e2, ctx->stream));
+  g_launches += 2;
+  return FB_OK;
+}
+
+// Output rows [r0, r1) of one image, in workspace-sized bands.
+template <typename T>
+int run_rows(fb_ctx* ctx, int kind, GpaArgs<T>& a, int band, int r0, int r1, int* bands) {
+  for (int b0 = r0; b0 < r1; b0 += band) {
+    int rc = launch_band<T>(ctx, kind, a, b0, std::min(band, r1 - b0));
+    if (rc != FB_OK) return rc;
+    ++*bands;
+  }
+  return FB_OK;
+}
+
+// One image of a call: where its data lives on the device and how it is chunked.
+struct Item {
+  const fb_image* in;
+  fb_image* out;
+  const void* f;  // device input
+  long long f_ld;
+  void* o;        // device output
+  long long o_ld;
+  int rows_out;
+  int chunks;
+};
+
+// Copy-in / filter / copy-out for `count` images.  Host-resident images are pipelined in
+// row chunks over three streams: H2D of chunk c+1 || kernels of chunk c || D2H of chunk c-1.
+// Kernels of a chunk wait for the input rows they read (chunk rows + W halo rows).
+template <typename T>
+int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bottom, const Job& j,
+              fb_stats* st) {
+  const bool validate_only = items[0].out == nullptr;
+  int band = 0;
+  GpaArgs<T> a;
+  int rows_max = 0;
+  for (auto& it : items) rows_max = std::max(rows_max, it.rows_out);
+  if (!validate_only) {
+    int rc = prepare<T>(ctx, j, (int)items[0].in->cols, rows_max, a, &band);
+    if (rc != FB_OK) return rc;
+  }
+  FB_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_start, 0));
+  FB_CUDA(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_start, 0));
+  std::vector<cudaEvent_t> img_done(items.size(), nullptr);  // compute finished with image i's buffers
+  std::vector<cudaEvent_t> out_done(items.size(), nullptr);  // D2H of image i finished
+  for (size_t i = 0; i < items.size(); ++i) {
+    Item& it = items[i];
+    const fb_image* in = it.in;
+    const size_t ies = dtype_size(in->dtype);
+    const int slot = (int)(i & 1);
+    const bool host_in = !in->on_device;
+    const bool host_out = it.out && !it.out->on_device;
+    // device buffers (double-buffered across images; reuse waits for image i-2)
+    if (host_in) {
+      int rc = grow(&ctx->in_stage[slot], &ctx->in_stage_bytes[slot], (size_t)in->rows * in->cols * ies);
+      if (rc != FB_OK) return rc;
+      it.f = ctx->in_stage[slot];
+      it.f_ld = in->cols;
+      if (i >= 2) FB_CUDA(cudaStreamWaitEvent(ctx->s_h2d, img_done[i - 2], 0));
+    } else {
+      it.f = in->data;
+      it.f_ld = in->ld;
+    }
+    if (it.out) {
+      const size_t oes = dtype_size(it.out->dtype);
+      if (host_out) {
+        int rc = grow(&ctx->out_stage[slot], &ctx->out_stage_bytes[slot], (size_t)it.rows_out * it.out->cols * oes);
+        if (rc != FB_OK) return rc;
+        it.o = ctx->out_stage[slot];
+        it.o_ld = it.out->cols;
+        if (i >= 2) FB_CUDA(cudaStreamWaitEvent(ctx->stream, out_done[i - 2], 0));
+      } else {
+        it.o = it.out->data;
+        it.o_ld = it.out->ld;
+      }
+    }
+    const int W = validate_only ? 0 : j.W;
+    const int nch = it.chunks;
+    const int crows = (it.rows_out + nch - 1) / nch;
+    long long copied = 0;  // input buffer rows already sent
+    for (int c = 0; c < nch; ++c) {
+      const int r0 = c * crows, r1 = std::min(it.rows_out, r0 + crows);
+      if (r0 >= r1) break;
+      if (host_in) {
+        // input buffer rows this chunk reads: [halo_top + r0 - W, halo_top + r1 + W) clamped
+        const long long need = std::min<long long>(in->rows, (long long)halo_top + r1 + W);
+        const long long hi = (r1 == it.rows_out) ? in->rows : need;  // the last chunk sends the rest
+        if (hi > copied) {
+          FB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(const_cast<void*>(it.f)) + copied * in->cols * ies,
+                                    in->cols * ies, static_cast<const char*>(in->data) + copied * in->ld * ies,
+                                    in->ld * ies, in->cols * ies, hi - copied, cudaMemcpyHostToDevice,
+                                    ctx->s_h2d));
+          if (st) st->h2d_bytes += (hi - copied) * in->cols * (long long)ies;
+          copied = hi;
+        }
+        cudaEvent_t e = ctx->next_pev();
+        FB_CUDA(cudaEventRecord(e, ctx->s_h2d));
+        FB_CUDA(cudaStreamWaitEvent(ctx->stream, e, 0));
+      }
+      if (validate_only) {
+        int rc = launch_validate(ctx->stream, it.f, it.f_ld, in->dtype, (int)in->rows, (int)in->cols, j.lo, j.hi,
+                                 ctx->flags + 4 * i, ctx->sm_count);
+        if (rc != FB_OK) return fail(FB_ERR_CUDA, "validation kernel launch failed");
+        g_launches += 1;
+      } else {
+        a.f = it.f;
+        a.f_ld = it.f_ld;
+        a.f_dtype = in->dtype;
+        a.rows_in = (int)in->rows;
+        a.halo_top = halo_top;
+        a.out = it.o;
+        a.out_ld = it.o_ld;
+        a.out_dtype = it.out->dtype;
+        a.flags = ctx->flags + 4 * i;
+        int nb = 0;
+        int rc = run_rows<T>(ctx, j.kind, a, band, r0, r1, &nb);
+        if (rc != FB_OK) return rc;
+        if (st) st->bands += nb;
+      }
+      if (host_out) {
+        cudaEvent_t e = ctx->next_pev();
+        FB_CUDA(cudaEventRecord(e, ctx->stream));
+        FB_CUDA(cudaStreamWaitEvent(ctx->s_d2h, e, 0));
+        const size_t oes = dtype_size(it.out->dtype);
+        FB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(it.out->data) + (size_t)r0 * it.out->ld * oes,
+                                  it.out->ld * oes, static_cast<char*>(it.o) + (size_t)r0 * it.o_ld * oes,
+                                  it.o_ld * oes, it.out->cols * oes, r1 - r0, cudaMemcpyDeviceToHost, ctx->s_d2h));
+        if (st) st->d2h_bytes += (long long)(r1 - r0) * it.out->cols * (long long)oes;
+      }
+    }
+    img_done[i] = ctx->next_pev();
+    FB_CUDA(cudaEventRecord(img_done[i], ctx->stream));
+    out_done[i] = ctx->next_pev();
+    FB_CUDA(cudaEventRecord(out_done[i], host_out ? ctx->s_d2h : ctx->stream));
+  }
+  // join the copy streams back into the compute stream
+  cudaEvent_t e1 = ctx->next_pev(), e2 = ctx->next_pev();
+  FB_CUDA(cudaEventRecord(e1, ctx->s_h2d));
+  FB_CUDA(cudaEventRecord(e2, ctx->s_d2h));
+  FB_CUDA(cudaStreamWaitEvent(ctx->stream, e1, 0));
+  FB_CUDA(cudaStreamWaitEvent(ctx->stream, e2, 0));
+  return FB_OK;
+}
+
+int ensure_flags(fb_ctx* ctx, int count) {
+  if (count <= ctx->flags_cap) return FB_OK;
+  if (ctx->flags) cudaFree(ctx->flags);
+  if (ctx->flags_host) cudaFreeHost(ctx->flags_host);
+  ctx->flags = nullptr;
+  ctx->flags_host = nullptr;
+  ctx->flags_cap = 0;
+  const int cap = std::max(count, 64);
+  FB_CUDA(cudaMalloc(&ctx->flags, 4 * sizeof(unsigned long long) * cap));
+  FB_CUDA(cudaMallocHost(&ctx->flags_host, 8 * sizeof(unsigned long long) * cap));
+  for (int i = 0; i < cap; ++i) {
+    unsigned long long* init = ctx->flags_host + 4 * i;  // first half: the reset pattern
+    init[kFlagFirstNonfinite] = ~0ull;
+    init[kFlagFirstRange] = ~0ull;
+    init[kFlagDegenerate] = 0;
+    init[kFlagNonfiniteOut] = 0;
+  }
+  ctx->flags_cap = cap;
+  return FB_OK;
+}
+
+// Run `count` images through the pipeline, read the flags back and map them to a status.
+int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int halo_top, int halo_bottom,
+            const Job& j, int precision, fb_stats* st) {
   FB_CUDA(cudaSetDevice(ctx->device));
   fb_stats local;
   memset(&local, 0, sizeof(local));
-  const size_t ies = dtype_size(in->dtype);
-  const long long rows_out = in->rows - halo_top - halo_bottom;
-  int rc;
-
-  FB_CUDA(cudaEventRecord(ctx->ev[0], ctx->stream));
-  // input
-  if (in->on_device) {
-    j.f = in->data;
-    j.f_ld = in->ld;
-  } else {
-    rc = grow(&ctx->in_stage, &ctx->in_stage_bytes, (size_t)in->rows * in->cols * ies);
-    if (rc != FB_OK) return rc;
-    FB_CUDA(cudaMemcpy2DAsync(ctx->in_stage, in->cols * ies, in->data, in->ld * ies, in->cols * ies, in->rows,
-                              cudaMemcpyHostToDevice, ctx->stream));
-    local.h2d_bytes += (long long)in->rows * in->cols * ies;
-    j.f = ctx->in_stage;
-    j.f_ld = in->cols;
-  }
-  // output
-  if (out) {
-    const size_t oes = dtype_size(out->dtype);
-    if (out->on_device) {
-      j.out = out->data;
-      j.out_ld = out->ld;
-    } else {
-      rc = grow(&ctx->out_stage, &ctx->out_stage_bytes, (size_t)rows_out * out->cols * oes);
-      if (rc != FB_OK) return rc;
-      j.out = ctx->out_stage;
-      j.out_ld = out->cols;
-    }
-    j.out_dtype = out->dtype;
-  }
-  j.f_dtype = in->dtype;
-  j.rows_in = (int)in->rows;
-  j.cols = (int)in->cols;
-  j.halo_top = halo_top;
-  j.rows_out = (int)rows_out;
-
-  FB_CUDA(cudaMemcpyAsync(ctx->flags, ctx->flags_host, 4 * sizeof(unsigned long long), cudaMemcpyHostToDevice,
-                          ctx->stream));
+  local.bad_image = -1;
+  int rc = ensure_flags(ctx, count);
+  if (rc != FB_OK) return rc;
   ctx->kev_used = 0;
-  const long long launches0 = g_launches.load();
-  FB_CUDA(cudaEventRecord(ctx->ev[1], ctx->stream));
-  if (out) {
-    rc = precision == FB_PREC_F64 ? run_job<double>(ctx, j, &local) : run_job<float>(ctx, j, &local);
-    if (rc != FB_OK) return rc;
-  } else {
-    rc = launch_validate(ctx->stream, j.f, j.f_ld, j.f_dtype, j.rows_in, j.cols, j.lo, j.hi, ctx->flags, ctx->sm_count);
-    if (rc != FB_OK) return rc;
-    g_launches += 1;
+  ctx->pev_used = 0;
+  FB_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
+  FB_CUDA(cudaMemcpyAsync(ctx->flags, ctx->flags_host, 4 * sizeof(unsigned long long) * count,
+                          cudaMemcpyHostToDevice, ctx->stream));
+  std::vector<Item> items(count);
+  long long pixels = 0;
+  for (int i = 0; i < count; ++i) {
+    Item& it = items[i];
+    memset(&it, 0, sizeof(it));
+    it.in = ins + i;
+    it.out = outs ? outs + i : nullptr;
+    it.rows_out = (int)(ins[i].rows - halo_top - halo_bottom);
+    pixels += (long long)it.rows_out * ins[i].cols;
+    // host images of more than 4 MP are pipelined in 8 row chunks
+    const bool host_io = !ins[i].on_device || (it.out && !it.out->on_device);
+    const long long px = (long long)it.rows_out * ins[i].cols;
+    it.chunks = (host_io && px >= (4ll << 20) && it.rows_out >= 512) ? 8 : 1;
   }
-  FB_CUDA(cudaEventRecord(ctx->ev[2], ctx->stream));
-  FB_CUDA(cudaMemcpyAsync(ctx->flags_host + 4, ctx->flags, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+  const long long launches0 = g_launches.load();
+  FB_CUDA(cudaEventRecord(ctx->ev_kstart, ctx->stream));
+  rc = precision == FB_PREC_F64 ? run_items<double>(ctx, items, halo_top, halo_bottom, j, &local)
+                                : run_items<float>(ctx, items, halo_top, halo_bottom, j, &local);
+  if (rc != FB_OK) return rc;
+  FB_CUDA(cudaEventRecord(ctx->ev_kend, ctx->stream));
+  unsigned long long* fl_all = ctx->flags_host + 4 * ctx->flags_cap;
+  FB_CUDA(cudaMemcpyAsync(fl_all, ctx->flags, 4 * sizeof(unsigned long long) * count, cudaMemcpyDeviceToHost,
                           ctx->stream));
-  FB_CUDA(cudaStreamSynchronize(ctx->stream));
-  const unsigned long long* fl = ctx->flags_host + 4;
+  FB_CUDA(cudaEventRecord(ctx->ev_end, ctx->stream));
+  FB_CUDA(cudaEventSynchronize(ctx->ev_end));
   local.launches = g_launches.load() - launches0;
   local.precision = precision;
-  local.degenerate_pixels = (long long)fl[kFlagDegenerate];
-  local.nonfinite_outputs = (long long)fl[kFlagNonfiniteOut];
 
-  auto sample_at = [&](unsigned long long idx) -> double {
-    const long long r = (long long)(idx / (unsigned long long)in->cols), c = (long long)(idx % in->cols);
-    const char* base = static_cast<const char*>(in->data) + ((size_t)r * in->ld + c) * ies;
-    unsigned char buf[8];
-    if (in->on_device) {
-      if (cudaMemcpy(buf, base, ies, cudaMemcpyDeviceToHost) != cudaSuccess) return NAN;
-    } else {
-      memcpy(buf, base, ies);
-    }
-    if (in->dtype == FB_U8) return (double)buf[0];
-    if (in->dtype == FB_F32) { float v; memcpy(&v, buf, 4); return (double)v; }
-    double v; memcpy(&v, buf, 8); return v;
-  };
   int status = FB_OK;
-  if (fl[kFlagFirstNonfinite] != ~0ull) {
-    local.bad_index = (long long)fl[kFlagFirstNonfinite];
-    local.bad_value = sample_at(fl[kFlagFirstNonfinite]);
-    status = fail(FB_ERR_NONFINITE_INPUT, "image contains non-finite samples");
-  } else if (fl[kFlagFirstRange] != ~0ull) {
-    local.bad_index = (long long)fl[kFlagFirstRange];
-    local.bad_value = sample_at(fl[kFlagFirstRange]);
-    status = fail(FB_ERR_RANGE, "sample outside the declared range");
-  } else if (out && fl[kFlagNonfiniteOut] != 0) {
-    status = fail(FB_ERR_NUMERIC, "non-finite output");
+  for (int i = 0; i < count && status == FB_OK; ++i) {
+    const unsigned long long* fl = fl_all + 4 * i;
+    const fb_image* in = ins + i;
+    const size_t ies = dtype_size(in->dtype);
+    local.degenerate_pixels += (long long)fl[kFlagDegenerate];
+    local.nonfinite_outputs += (long long)fl[kFlagNonfiniteOut];
+    auto sample_at = [&](unsigned long long idx) -> double {
+      const long long r = (long long)(idx / (unsigned long long)in->cols), c = (long long)(idx % in->cols);
+      const char* base = static_cast<const char*>(in->data) + ((size_t)r * in->ld + c) * ies;
+      unsigned char buf[8];
+      if (in->on_device) {
+        if (cudaMemcpy(buf, base, ies, cudaMemcpyDeviceToHost) != cudaSuccess) return NAN;
+      } else {
+        memcpy(buf, base, ies);
+      }
+      if (in->dtype == FB_U8) return (double)buf[0];
+      if (in->dtype == FB_F32) { float v; memcpy(&v, buf, 4); return (double)v; }
+      double v; memcpy(&v, buf, 8); return v;
+    };
+    if (fl[kFlagFirstNonfinite] != ~0ull) {
+      local.bad_index = (long long)fl[kFlagFirstNonfinite];
+      local.bad_value = sample_at(fl[kFlagFirstNonfinite]);
+      local.bad_image = i;
+      status = fail(FB_ERR_NONFINITE_INPUT, "image contains non-finite samples");
+    } else if (fl[kFlagFirstRange] != ~0ull) {
+      local.bad_index = (long long)fl[kFlagFirstRange];
+      local.bad_value = sample_at(fl[kFlagFirstRange]);
+      local.bad_image = i;
+      status = fail(FB_ERR_RANGE, "sample outside the declared range");
+    } else if (outs && fl[kFlagNonfiniteOut] != 0) {
+      local.bad_image = i;
+      status = fail(FB_ERR_NUMERIC, "non-finite output");
+    }
   }
-  if (status == FB_OK && out && !out->on_device) {
-    const size_t oes = dtype_size(out->dtype);
-    FB_CUDA(cudaMemcpy2DAsync(out->data, out->ld * oes, j.out, j.out_ld * oes, out->cols * oes, rows_out,
-                              cudaMemcpyDeviceToHost, ctx->stream));
-    local.d2h_bytes += rows_out * out->cols * (long long)oes;
-  }
-  FB_CUDA(cudaEventRecord(ctx->ev[3], ctx->stream));
-  FB_CUDA(cudaEventSynchronize(ctx->ev[3]));
   float ms = 0.f, kms = 0.f;
-  cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[3]);
-  cudaEventElapsedTime(&kms, ctx->ev[1], ctx->ev[2]);
+  cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_end);
+  cudaEventElapsedTime(&kms, ctx->ev_kstart, ctx->ev_kend);
   local.device_ms = ms;
   local.kernel_ms = kms;
   for (int b = 0; b + 2 < ctx->kev_used; b += 3) {
@@ -345,6 +490,7 @@ int execute(fb_ctx* ctx, const fb_image* in, int halo_top, int halo_bottom, fb_i
   }
   local.spatial_filter_calls = j.N + 1;
   local.order = j.mode == kModeGpa ? j.N : 0;
+  (void)pixels;
   if (st) *st = local;
   return status;
 }
@@ -367,18 +513,16 @@ int fb_create(int device, fb_ctx** out) {
   fb_ctx* c = new fb_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
-  if (cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaMalloc(&c->flags, 4 * sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMallocHost(&c->flags_host, 8 * sizeof(unsigned long long)) != cudaSuccess) {
-    fb_destroy(c);
-    return fail(FB_ERR_CUDA, "fb_create: stream/flag allocation failed");
-  }
-  for (auto& e : c->ev) cudaEventCreate(&e);
+  bool ok = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking) == cudaSuccess;
+  for (cudaEvent_t* e : {&c->ev_start, &c->ev_kstart, &c->ev_kend, &c->ev_end})
+    ok = ok && cudaEventCreate(e) == cudaSuccess;
   c->stream = c->own_stream;
-  c->flags_host[0] = ~0ull;
-  c->flags_host[1] = ~0ull;
-  c->flags_host[2] = 0;
-  c->flags_host[3] = 0;
+  if (!ok || ensure_flags(c, 64) != FB_OK) {
+    fb_destroy(c);
+    return fail(FB_ERR_CUDA, "fb_create: stream/event/flag allocation failed");
+  }
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   c->ws_limit = std::min<long long>(16ll << 30, (long long)(free_b / 4));
@@ -389,17 +533,18 @@ int fb_create(int device, fb_ctx** out) {
 int fb_destroy(fb_ctx* c) {
   if (!c) return FB_OK;
   cudaSetDevice(c->device);
-  if (c->ws) cudaFree(c->ws);
-  if (c->in_stage) cudaFree(c->in_stage);
-  if (c->out_stage) cudaFree(c->out_stage);
-  if (c->flags) cudaFree(c->flags);
-  if (c->flags_host) cudaFreeHost(c->flags_host);
-  if (c->tab) cudaFree(c->tab);
-  if (c->tab_host) cudaFreeHost(c->tab_host);
-  for (auto& e : c->ev)
+  if (c->own_stream) cudaStreamSynchronize(c->own_stream);
+  for (void* p : {c->ws, c->in_stage[0], c->in_stage[1], c->out_stage[0], c->out_stage[1], (void*)c->flags,
+                  (void*)c->tab, (void*)c->tabd})
+    if (p) cudaFree(p);
+  for (void* p : {(void*)c->flags_host, (void*)c->tab_host, (void*)c->tabd_host})
+    if (p) cudaFreeHost(p);
+  for (cudaEvent_t e : {c->ev_start, c->ev_kstart, c->ev_kend, c->ev_end})
     if (e) cudaEventDestroy(e);
   for (auto& e : c->kev) cudaEventDestroy(e);
-  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  for (auto& e : c->pev) cudaEventDestroy(e);
+  for (cudaStream_t s : {c->own_stream, c->s_h2d, c->s_d2h})
+    if (s) cudaStreamDestroy(s);
   delete c;
   return FB_OK;
 }
@@ -438,25 +583,29 @@ static int check_window(const fb_spatial* sp, long long rows, long long cols) {
   return FB_OK;
 }
 
-int fb_gpa_filter(fb_ctx* ctx, const fb_image* in, int64_t halo_top, int64_t halo_bottom, fb_image* out,
-                  const fb_spatial* sp, double sigma_r, int32_t order, double center, double half_range,
-                  int32_t precision, fb_stats* stats) {
+static int gpa_common(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int64_t halo_top,
+                      int64_t halo_bottom, const fb_spatial* sp, double sigma_r, int32_t order, double center,
+                      double half_range, int32_t precision, fb_stats* stats) {
   if (!ctx) return fail(FB_ERR_PARAM, "null context");
-  int rc = check_image(in, "input", true);
+  if (count < 1 || !ins || !outs) return fail(FB_ERR_PARAM, "need at least one image");
+  int rc = check_filter_args(sp, precision);
   if (rc) return rc;
-  rc = check_image(out, "output", false);
-  if (rc) return rc;
-  rc = check_filter_args(sp, precision);
-  if (rc) return rc;
-  if (halo_top < 0 || halo_bottom < 0 || halo_top + halo_bottom >= in->rows)
-    return fail(FB_ERR_PARAM, "bad halo rows");
-  const long long rows_out = in->rows - halo_top - halo_bottom;
-  if (out->rows != rows_out || out->cols != in->cols) return fail(FB_ERR_PARAM, "output shape mismatch");
   if (!(sigma_r > 0) || !std::isfinite(sigma_r)) return fail(FB_ERR_PARAM, "sigma_r must be positive");
   if (order < 1) return fail(FB_ERR_PARAM, "order must be an integer >= 1");
   if (!(half_range > 0)) return fail(FB_ERR_PARAM, "half_range must be positive");
-  rc = check_window(sp, rows_out, in->cols);
-  if (rc) return rc;
+  for (int i = 0; i < count; ++i) {
+    rc = check_image(ins + i, "input", true);
+    if (rc) return rc;
+    rc = check_image(outs + i, "output", false);
+    if (rc) return rc;
+    if (halo_top < 0 || halo_bottom < 0 || halo_top + halo_bottom >= ins[i].rows)
+      return fail(FB_ERR_PARAM, "bad halo rows");
+    if (ins[i].cols != ins[0].cols) return fail(FB_ERR_PARAM, "images of a batch must share their width");
+    const long long rows_out = ins[i].rows - halo_top - halo_bottom;
+    if (outs[i].rows != rows_out || outs[i].cols != ins[i].cols) return fail(FB_ERR_PARAM, "output shape mismatch");
+    rc = check_window(sp, rows_out, ins[i].cols);
+    if (rc) return rc;
+  }
   Job j;
   memset(&j, 0, sizeof(j));
   j.kind = sp->kind;
@@ -469,7 +618,20 @@ int fb_gpa_filter(fb_ctx* ctx, const fb_image* in, int64_t halo_top, int64_t hal
   j.tc = center;
   j.lo = center - half_range;
   j.hi = center + half_range;
-  return execute(ctx, in, (int)halo_top, (int)halo_bottom, out, j, precision, stats);
+  return execute(ctx, ins, outs, count, (int)halo_top, (int)halo_bottom, j, precision, stats);
+}
+
+int fb_gpa_filter(fb_ctx* ctx, const fb_image* in, int64_t halo_top, int64_t halo_bottom, fb_image* out,
+                  const fb_spatial* sp, double sigma_r, int32_t order, double center, double half_range,
+                  int32_t precision, fb_stats* stats) {
+  return gpa_common(ctx, in, out, 1, halo_top, halo_bottom, sp, sigma_r, order, center, half_range, precision,
+                    stats);
+}
+
+int fb_gpa_filter_batch(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int32_t count, const fb_spatial* sp,
+                        double sigma_r, int32_t order, double center, double half_range, int32_t precision,
+                        fb_stats* stats) {
+  return gpa_common(ctx, ins, outs, count, 0, 0, sp, sigma_r, order, center, half_range, precision, stats);
 }
 
 int fb_spatial_filter(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_spatial* sp, int32_t precision,
@@ -494,7 +656,7 @@ int fb_spatial_filter(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_s
   j.tc = 0.0;
   j.lo = -INFINITY;
   j.hi = INFINITY;
-  return execute(ctx, in, 0, 0, out, j, precision, stats);
+  return execute(ctx, in, out, 1, 0, 0, j, precision, stats);
 }
 
 int fb_validate(fb_ctx* ctx, const fb_image* in, double lo, double hi, fb_stats* stats) {
@@ -505,7 +667,7 @@ int fb_validate(fb_ctx* ctx, const fb_image* in, double lo, double hi, fb_stats*
   memset(&j, 0, sizeof(j));
   j.lo = lo;
   j.hi = hi;
-  return execute(ctx, in, 0, 0, nullptr, j, FB_PREC_F64, stats);
+  return execute(ctx, in, nullptr, 1, 0, 0, j, FB_PREC_F64, stats);
 }
 
 }  // extern "C"

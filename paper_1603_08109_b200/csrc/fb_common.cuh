@@ -59,7 +59,11 @@ struct GpaArgs {
   long long out_ld;
   int out_dtype;      // 1 f32, 2 f64
   unsigned long long* flags;
-  const float* tab;   // fp32 channel constants: tab[2m] = 1/sqrt(m) (0 for m = 0), tab[2m+1] = sqrt(m)
+  // fp32 channel constants, 4 per channel m: r_m = fl32(1/sqrt(m)) (0 for m = 0), sqrt(m),
+  // and the matched Horner constants h_m = 1/(m r_m), s_m = 1/r_m rounded to fp32
+  const float* tab;
+  // fp64 Horner constants matched to r_m (see k2f_hpass_horner): tabd[2m] = 1/(m r_m), tabd[2m+1] = 1/r_m
+  const double* tabd;
   T w[kMaxTaps];      // normalised 1-D taps (gaussian)
   // Tap pairs for packed FFMA2 (fp32 fast path): wq[2a] = w[a], wq[2a+1] = w[a-1],
   // a = 0 .. 2W+1, with w[-1] = w[2W+1] = 0 (box: all ones).

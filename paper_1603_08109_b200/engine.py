@@ -154,7 +154,52 @@ def gpa_filter(img, spatial: SpatialKernel, sigma_r: float, order: int,
         stats["k2_ms"] = st["k2_ms"]
         stats["launches"] = st["launches"]
         stats["bands"] = st["bands"]
+        stats["h2d_bytes"] = st["h2d_bytes"]
+        stats["d2h_bytes"] = st["d2h_bytes"]
     return out
+
+
+def gpa_filter_batch(images, spatial: SpatialKernel, sigma_r: float, order: int,
+                     range_spec: RangeSpec | None = None, *, allow_small_sigma: bool = False,
+                     stats: dict | None = None, precision: str = "auto", device: int | None = None,
+                     out_dtype=np.float64, outs=None) -> list:
+    """`gpa_filter` over a batch of equally wide images in one call (by-image partitioning, config c3).
+
+    Host-resident images are pipelined (copy-in of image i+1 and copy-out of image i-1 overlap
+    the kernels of image i).  Returns the list of outputs; errors name the offending image.
+    """
+    arrs = [_coerce(im) for im in images]
+    if not arrs:
+        return []
+    is_dev = arrs[0][1]
+    if any(d != is_dev for _, d in arrs):
+        raise ParameterError("a batch must be all host arrays or all CUDA tensors")
+    arrs = [a for a, _ in arrs]
+    shapes = [_shape_check(a) for a in arrs]
+    if len({s[1] for s in shapes}) != 1:
+        raise ParameterError("images of a batch must share their width")
+    if range_spec is None:
+        range_spec = RangeSpec(half_range=128.0, center=128.0)
+    if not (sigma_r > 0) or (sigma_r < SIGMA_R_FLOOR and not allow_small_sigma) or \
+            not (isinstance(order, (int, np.integer)) or float(order).is_integer()) or order < 1 or \
+            any(_window_error(spatial, s) for s in shapes):
+        # single-image path raises exactly the reference's errors in the reference's order
+        for a in arrs:
+            gpa_filter(a, spatial, sigma_r, order, range_spec, allow_small_sigma=allow_small_sigma,
+                       precision=precision, device=device)
+    dev = _native.device_of(arrs[0], device)
+    prec = resolve_precision(precision, min(shapes, key=lambda s: s[0] * s[1]), sigma_r)
+    if outs is None:
+        outs = [_alloc_out(a, is_dev, s, out_dtype) for a, s in zip(arrs, shapes)]
+    st = _native.gpa_batch(arrs, outs, spatial, float(sigma_r), int(order), range_spec.center,
+                           range_spec.half_range, prec, dev)
+    if stats is not None:
+        stats.update({k: st[k] for k in ("degenerate_pixels", "device_ms", "kernel_ms", "k1_ms", "k2_ms",
+                                         "launches", "bands", "h2d_bytes", "d2h_bytes")})
+        stats["spatial_filter_calls"] = int(order) + 1
+        stats["order"] = int(order)
+        stats["precision"] = "f64" if st["precision"] == _native.FB_PREC_F64 else "f32"
+    return outs
 
 
 def gpa_filter_auto(img, spatial: SpatialKernel, sigma_r: float, delta: float,

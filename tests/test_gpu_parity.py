@@ -140,6 +140,39 @@ def test_row_bands_bit_exact():
         assert np.array_equal(full, banded)
 
 
+def test_batch_matches_single_and_names_bad_image():
+    from paper_1603_08109_b200 import gpa_filter_batch
+    rng = np.random.default_rng(21)
+    imgs = [np.floor(rng.uniform(0.0, 256.0, (h, 260))).astype(np.float32) for h in (300, 257, 64, 300)]
+    k = make_spatial_kernel("gaussian", sigma_s=3.0)
+    stats = {}
+    outs = gpa_filter_batch(imgs, k, 40.0, 15, stats=stats, precision="f32")
+    assert stats["launches"] == 2 * len(imgs)
+    for im, o in zip(imgs, outs):
+        assert np.array_equal(o, gpa_filter(im, k, 40.0, 15, precision="f32"))
+    bad = [im.copy() for im in imgs]
+    bad[2][5, 7] = 300.0
+    with pytest.raises(RangeViolationError, match=r"row=5, col=7"):
+        gpa_filter_batch(bad, k, 40.0, 15, precision="f32")
+
+
+def test_chunked_host_pipeline_matches_device_path():
+    """Host images > 4 MP are pipelined in 8 row chunks over three streams.  The box walker's
+    running sums restart at chunk boundaries, so both partitions are compared with the fp64 path
+    (itself pinned to the reference at 1e-9) rather than with each other bitwise."""
+    torch = pytest.importorskip("torch")
+    cfg = synth.CONFIGS["c4"]
+    img = synth.config_image(cfg, height=2304, width=2048)
+    for k, N in ((synth.config_kernel(cfg), 57), (make_spatial_kernel("gaussian", sigma_s=5.0), 42)):
+        stats = {}
+        host = gpa_filter(img, k, 25.0, N, precision="f32", stats=stats)
+        assert stats["h2d_bytes"] == img.nbytes and stats["d2h_bytes"] == host.nbytes
+        dev = gpa_filter(torch.from_numpy(img).cuda(), k, 25.0, N, precision="f32").cpu().numpy()
+        ref = gpa_filter(img, k, 25.0, N, precision="f64")
+        assert np.max(np.abs(host - ref)) <= 5e-4
+        assert np.max(np.abs(dev - ref)) <= 5e-4
+
+
 def test_cuda_tensor_in_tensor_out():
     torch = pytest.importorskip("torch")
     rng = np.random.default_rng(14)

@@ -34,7 +34,7 @@ def test_struct_layouts():
     # int64-aligned C structs: sizes must match the header's field lists.
     assert ctypes.sizeof(_native.FbImage) == 8 + 4 + 4 + 8 * 3
     assert ctypes.sizeof(_native.FbSpatial) == 4 + 4 + 8
-    assert ctypes.sizeof(_native.FbStats) == 8 * 12 + 4 + 4 + 8
+    assert ctypes.sizeof(_native.FbStats) == 8 * 12 + 4 + 4 + 8 + 8
 
 
 def test_no_gpu_fails_loudly():
