@@ -45,6 +45,9 @@ struct fb_ctx {
   cudaStream_t own_stream = nullptr;
   cudaStream_t s_h2d = nullptr;       // host -> device copies of the pipelined host path
   cudaStream_t s_d2h = nullptr;       // device -> host copies
+  cudaStream_t s_alt = nullptr;       // second compute stream: odd images of a batch
+  void* ws2 = nullptr;                // its workspace
+  size_t ws2_bytes = 0;
   void* ws = nullptr;                 // channel planes of one row band
   size_t ws_bytes = 0;
   void* in_stage[2] = {nullptr, nullptr};   // device copies of host inputs (double-buffered per image)
@@ -116,6 +119,19 @@ struct Job {
   double sr, tc, lo, hi;
 };
 
+// Order that Algorithm 1 (order.py:91-153) selects for a per-pixel error of delta = 1 gray level:
+// the smallest N > lambda whose Chernoff bound meets eps = w0 / (2T + 1) (exhaustive scan; the
+// Lambert-W estimate agrees to +-1, tests/test_order.py).  Used only for the Horner-precision policy.
+int order_delta1(double sigma_r, double w0, double T) {
+  const double eps = w0 / (2.0 * T + 1.0);
+  const double lam = (T / sigma_r) * (T / sigma_r);
+  if (sigma_r >= 70.0) return 10;
+  if (!(eps > 0.0 && eps < 1.0)) return 0;
+  int n = (int)std::floor(lam) + 1;
+  while (n < 100000 && -lam + n * (1.0 + std::log(lam) - std::log((double)n)) > std::log(eps)) ++n;
+  return n;
+}
+
 // The precision-typed argument block: constants once per call, pointers per image.
 template <typename T>
 int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a, int* band_out) {
@@ -131,6 +147,10 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
   a.hi = j.hi;
   a.cols = cols;
   const int n_taps = 2 * j.W + 1;
+  {
+    const double w0 = j.kind == FB_BOX ? 1.0 / ((double)n_taps * n_taps) : j.taps[j.W] * j.taps[j.W];
+    a.n_delta1 = j.mode == kModeGpa ? order_delta1(j.sr, w0, (j.hi - j.lo) / 2.0) : 0;
+  }
   if (j.kind == FB_BOX) {
     a.norm = (T)(1.0 / ((double)n_taps * n_taps));
     for (int k = 0; k < n_taps; ++k) a.w[k] = T(1);
@@ -144,8 +164,13 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
       a.wq[2 * q + 1] = q > 0 ? (float)a.w[q - 1] : 0.f;
     }
   }
-  for (int m = 0; m < kWalkMaxCh; ++m)
-    a.rsc2[2 * m] = a.rsc2[2 * m + 1] = m > 0 ? (float)(1.0 / std::sqrt((double)m)) : 0.f;
+  double a32 = 1.0;
+  for (int m = 0; m < kWalkMaxCh; ++m) {
+    const float r = m > 0 ? (float)(1.0 / std::sqrt((double)m)) : 0.f;
+    a.rsc2[2 * m] = a.rsc2[2 * m + 1] = r;
+    if (m >= 1 && m <= 32) a32 *= (double)r;
+  }
+  a.walk_a32 = (float)a32;
   // channel constants 1/sqrt(m), sqrt(m) (rounded once from double), uploaded when N changes
   if (j.N + 1 > ctx->tab_cap) {
     for (void* p : {(void*)ctx->tab, (void*)ctx->tabd}) if (p) cudaFree(p);
@@ -205,14 +230,14 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
 }
 
 template <typename T>
-int launch_band(fb_ctx* ctx, int kind, GpaArgs<T>& a, int band_row0, int band_rows) {
+int launch_band(fb_ctx* ctx, cudaStream_t st, int kind, GpaArgs<T>& a, int band_row0, int band_rows) {
   a.band_row0 = band_row0;
   a.band_rows = band_rows;
   const int W = a.W;
   bool done = false;
   cudaEvent_t e0 = ctx->next_kev(), e1 = ctx->next_kev(), e2 = ctx->next_kev();
   KernelEvents kev{e0, e1, e2};
-  int rc = launch_fast<T>(ctx->stream, kind, W, a, kev, &done);
+  int rc = launch_fast<T>(st, kind, W, a, kev, &done);
   if (rc != FB_OK) return fail(FB_ERR_CUDA, std::string("fast kernel launch failed: ") +
                                                cudaGetErrorString(cudaGetLastError()));
   if (done) {
@@ -226,22 +251,22 @@ int launch_band(fb_ctx* ctx, int kind, GpaArgs<T>& a, int band_row0, int band_ro
   auto k2 = kind == FB_BOX ? generic::k2_hpass_horner<T, kKindBox> : generic::k2_hpass_horner<T, kKindGauss>;
   FB_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
   FB_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
-  FB_CUDA(cudaEventRecord(e0, ctx->stream));
-  k1<<<g1, generic::K1_TC * generic::K1_RG, s1, ctx->stream>>>(a);
+  FB_CUDA(cudaEventRecord(e0, st));
+  k1<<<g1, generic::K1_TC * generic::K1_RG, s1, st>>>(a);
   FB_CUDA(cudaGetLastError());
-  FB_CUDA(cudaEventRecord(e1, ctx->stream));
-  k2<<<g2, 256, s2, ctx->stream>>>(a);
+  FB_CUDA(cudaEventRecord(e1, st));
+  k2<<<g2, 256, s2, st>>>(a);
   FB_CUDA(cudaGetLastError());
-  FB_CUDA(cudaEventRecord(e2, ctx->stream));
+  FB_CUDA(cudaEventRecord(e2, st));
   g_launches += 2;
   return FB_OK;
 }
 
 // Output rows [r0, r1) of one image, in workspace-sized bands.
 template <typename T>
-int run_rows(fb_ctx* ctx, int kind, GpaArgs<T>& a, int band, int r0, int r1, int* bands) {
+int run_rows(fb_ctx* ctx, cudaStream_t st, int kind, GpaArgs<T>& a, int band, int r0, int r1, int* bands) {
   for (int b0 = r0; b0 < r1; b0 += band) {
-    int rc = launch_band<T>(ctx, kind, a, b0, std::min(band, r1 - b0));
+    int rc = launch_band<T>(ctx, st, kind, a, b0, std::min(band, r1 - b0));
     if (rc != FB_OK) return rc;
     ++*bands;
   }
@@ -275,6 +300,19 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
     int rc = prepare<T>(ctx, j, (int)items[0].in->cols, rows_max, a, &band);
     if (rc != FB_OK) return rc;
   }
+  // Batches alternate images between two compute streams with two workspaces, so the kernels
+  // of image i+1 fill the tail waves of image i.
+  const bool dual = !validate_only && items.size() > 1;
+  cudaStream_t cs[2] = {ctx->stream, dual ? ctx->s_alt : ctx->stream};
+  T* wsp[2] = {a.v, a.v};
+  if (dual) {
+    int rc = grow(&ctx->ws2, &ctx->ws2_bytes, (size_t)band * a.rstride * sizeof(T));
+    if (rc != FB_OK) return rc;
+    wsp[1] = reinterpret_cast<T*>(ctx->ws2);
+    cudaEvent_t e = ctx->next_pev();  // after the constant-table upload in prepare()
+    FB_CUDA(cudaEventRecord(e, ctx->stream));
+    FB_CUDA(cudaStreamWaitEvent(ctx->s_alt, e, 0));
+  }
   FB_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_start, 0));
   FB_CUDA(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_start, 0));
   std::vector<cudaEvent_t> img_done(items.size(), nullptr);  // compute finished with image i's buffers
@@ -284,6 +322,7 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
     const fb_image* in = it.in;
     const size_t ies = dtype_size(in->dtype);
     const int slot = (int)(i & 1);
+    cudaStream_t cstr = cs[slot];
     const bool host_in = !in->on_device;
     const bool host_out = it.out && !it.out->on_device;
     // device buffers (double-buffered across images; reuse waits for image i-2)
@@ -304,7 +343,7 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
         if (rc != FB_OK) return rc;
         it.o = ctx->out_stage[slot];
         it.o_ld = it.out->cols;
-        if (i >= 2) FB_CUDA(cudaStreamWaitEvent(ctx->stream, out_done[i - 2], 0));
+        if (i >= 2) FB_CUDA(cudaStreamWaitEvent(cstr, out_done[i - 2], 0));
       } else {
         it.o = it.out->data;
         it.o_ld = it.out->ld;
@@ -331,10 +370,10 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
         }
         cudaEvent_t e = ctx->next_pev();
         FB_CUDA(cudaEventRecord(e, ctx->s_h2d));
-        FB_CUDA(cudaStreamWaitEvent(ctx->stream, e, 0));
+        FB_CUDA(cudaStreamWaitEvent(cstr, e, 0));
       }
       if (validate_only) {
-        int rc = launch_validate(ctx->stream, it.f, it.f_ld, in->dtype, (int)in->rows, (int)in->cols, j.lo, j.hi,
+        int rc = launch_validate(cstr, it.f, it.f_ld, in->dtype, (int)in->rows, (int)in->cols, j.lo, j.hi,
                                  ctx->flags + 4 * i, ctx->sm_count);
         if (rc != FB_OK) return fail(FB_ERR_CUDA, "validation kernel launch failed");
         g_launches += 1;
@@ -348,14 +387,15 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
         a.out_ld = it.o_ld;
         a.out_dtype = it.out->dtype;
         a.flags = ctx->flags + 4 * i;
+        a.v = wsp[slot];
         int nb = 0;
-        int rc = run_rows<T>(ctx, j.kind, a, band, r0, r1, &nb);
+        int rc = run_rows<T>(ctx, cstr, j.kind, a, band, r0, r1, &nb);
         if (rc != FB_OK) return rc;
         if (st) st->bands += nb;
       }
       if (host_out) {
         cudaEvent_t e = ctx->next_pev();
-        FB_CUDA(cudaEventRecord(e, ctx->stream));
+        FB_CUDA(cudaEventRecord(e, cstr));
         FB_CUDA(cudaStreamWaitEvent(ctx->s_d2h, e, 0));
         const size_t oes = dtype_size(it.out->dtype);
         FB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(it.out->data) + (size_t)r0 * it.out->ld * oes,
@@ -365,16 +405,20 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
       }
     }
     img_done[i] = ctx->next_pev();
-    FB_CUDA(cudaEventRecord(img_done[i], ctx->stream));
+    FB_CUDA(cudaEventRecord(img_done[i], cstr));
     out_done[i] = ctx->next_pev();
-    FB_CUDA(cudaEventRecord(out_done[i], host_out ? ctx->s_d2h : ctx->stream));
+    FB_CUDA(cudaEventRecord(out_done[i], host_out ? ctx->s_d2h : cstr));
   }
-  // join the copy streams back into the compute stream
-  cudaEvent_t e1 = ctx->next_pev(), e2 = ctx->next_pev();
+  // join the copy streams and the second compute stream back into the main stream
+  cudaEvent_t e1 = ctx->next_pev(), e2 = ctx->next_pev(), e3 = ctx->next_pev();
   FB_CUDA(cudaEventRecord(e1, ctx->s_h2d));
   FB_CUDA(cudaEventRecord(e2, ctx->s_d2h));
   FB_CUDA(cudaStreamWaitEvent(ctx->stream, e1, 0));
   FB_CUDA(cudaStreamWaitEvent(ctx->stream, e2, 0));
+  if (dual) {
+    FB_CUDA(cudaEventRecord(e3, ctx->s_alt));
+    FB_CUDA(cudaStreamWaitEvent(ctx->stream, e3, 0));
+  }
   return FB_OK;
 }
 
@@ -515,7 +559,8 @@ int fb_create(int device, fb_ctx** out) {
   cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device);
   bool ok = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking) == cudaSuccess &&
             cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking) == cudaSuccess &&
-            cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking) == cudaSuccess;
+            cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&c->s_alt, cudaStreamNonBlocking) == cudaSuccess;
   for (cudaEvent_t* e : {&c->ev_start, &c->ev_kstart, &c->ev_kend, &c->ev_end})
     ok = ok && cudaEventCreate(e) == cudaSuccess;
   c->stream = c->own_stream;
@@ -534,7 +579,7 @@ int fb_destroy(fb_ctx* c) {
   if (!c) return FB_OK;
   cudaSetDevice(c->device);
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
-  for (void* p : {c->ws, c->in_stage[0], c->in_stage[1], c->out_stage[0], c->out_stage[1], (void*)c->flags,
+  for (void* p : {c->ws, c->ws2, c->in_stage[0], c->in_stage[1], c->out_stage[0], c->out_stage[1], (void*)c->flags,
                   (void*)c->tab, (void*)c->tabd})
     if (p) cudaFree(p);
   for (void* p : {(void*)c->flags_host, (void*)c->tab_host, (void*)c->tabd_host})
@@ -543,7 +588,7 @@ int fb_destroy(fb_ctx* c) {
     if (e) cudaEventDestroy(e);
   for (auto& e : c->kev) cudaEventDestroy(e);
   for (auto& e : c->pev) cudaEventDestroy(e);
-  for (cudaStream_t s : {c->own_stream, c->s_h2d, c->s_d2h})
+  for (cudaStream_t s : {c->own_stream, c->s_h2d, c->s_d2h, c->s_alt})
     if (s) cudaStreamDestroy(s);
   delete c;
   return FB_OK;

@@ -71,6 +71,8 @@ struct GpaArgs {
   // (1/sqrt(n), 1/sqrt(n)) pairs for n < kWalkMaxCh, compile-time-indexed by the box walker
   alignas(8) float rsc2[2 * 64];
   int walk_rows;      // output rows per thread of the box walker
+  float walk_a32;     // prod_{k=1..32} r_k (start of the second channel half of the box walker)
+  int n_delta1;       // order Algorithm 1 picks for delta = 1 gray level (Horner-precision policy)
 };
 
 constexpr int kWalkMaxCh = 64;              // channels (N+1) the register-resident box walker holds
