@@ -15,6 +15,39 @@
 #include "fb_generic.cuh"
 #include "fb_fast.cuh"
 
+namespace fbgpu {
+// ============================================================================ validation
+__global__ void __launch_bounds__(256) k_validate(const void* f, long long ld, int dt, int rows, int cols,
+                                                  double lo, double hi, unsigned long long* flags) {
+  const long long total = (long long)rows * cols;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // Uniform trip count per warp so the ballot in flag_min sees full warps.
+  const long long base0 = (long long)blockIdx.x * blockDim.x;
+  for (long long base = base0; base < total; base += stride) {
+    const long long i = base + threadIdx.x;
+    const bool act = i < total;
+    double v = 0.0;
+    unsigned long long idx = 0;
+    if (act) {
+      const long long r = i / cols, c = i - r * cols;
+      v = load_sample(f, dt, r * ld + c);
+      idx = (unsigned long long)i;
+    }
+    check_sample(flags, act, v, lo, hi, idx);
+  }
+}
+
+int launch_validate(cudaStream_t s, const void* f, long long ld, int dt, int rows, int cols, double lo,
+                           double hi, unsigned long long* flags, int sms) {
+  const long long total = (long long)rows * cols;
+  long long blocks = (total + 255) / 256;
+  blocks = blocks < (long long)sms * 8 ? blocks : (long long)sms * 8;
+  k_validate<<<(int)blocks, 256, 0, s>>>(f, ld, dt, rows, cols, lo, hi, flags);
+  return cudaGetLastError() == cudaSuccess ? 0 : 6;
+}
+
+}  // namespace fbgpu
+
 using namespace fbgpu;
 
 namespace {
