@@ -152,6 +152,15 @@ int fb_spatial_filter(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_s
  */
 int fb_validate(fb_ctx* ctx, const fb_image* in, double lo, double hi, fb_stats* stats);
 
+/*
+ * fb_bilateral_exact — replaces bilateral_exact (reference.py:17-45): the exact O(W^2)
+ * bilateral filter in fp64 with replicate boundary, the oracle the GPA approximation error is
+ * measured against.  `out` must be FB_F64.  FB_ERR_WINDOW if W >= min(rows, cols)
+ * (reference.py:28-31).
+ */
+int fb_bilateral_exact(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_spatial* spatial,
+                       double sigma_r, fb_stats* stats);
+
 /* Message of the last failure on this host thread. */
 const char* fb_last_error(void);
 int fb_version(void);

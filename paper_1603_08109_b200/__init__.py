@@ -15,6 +15,7 @@ from .errors import (BoundInapplicableError, NativeError, NumericRangeError, Par
                      RangeViolationError)
 from .image import RANGE_8BIT, RangeSpec, as_image, center, uncenter, validate_range
 from .kernels import SpatialKernel, make_spatial_kernel
+from .reference import bilateral_exact
 from .order import (OrderEstimate, chernoff_order_exhaustive, epsilon_from_delta, estimate_order,
                     lambert_w0_series, log_chernoff)
 
@@ -22,7 +23,7 @@ __version__ = "1.0.0"
 
 __all__ = [
     "OrderEstimate", "RangeSpec", "SpatialKernel", "RANGE_8BIT", "__version__",
-    "apply_spatial", "as_image", "box_filter", "center", "chernoff_order_exhaustive",
+    "apply_spatial", "as_image", "bilateral_exact", "box_filter", "center", "chernoff_order_exhaustive",
     "epsilon_from_delta", "estimate_order", "gaussian_filter", "gpa_filter", "gpa_filter_auto",
     "gpa_filter_batch",
     "lambert_w0_series", "log_chernoff", "make_spatial_kernel", "uncenter", "validate_range",

@@ -28,8 +28,8 @@ FB_PREC_F32, FB_PREC_F64 = 1, 2
 #: Every symbol include/fbgpu.h declares (checked by tests/test_native_abi.py).
 EXPORTED_SYMBOLS = (
     "fb_create", "fb_destroy", "fb_set_stream", "fb_set_workspace_limit", "fb_gpa_filter",
-    "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate", "fb_last_error", "fb_version",
-    "fb_launch_count",
+    "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate", "fb_bilateral_exact", "fb_last_error",
+    "fb_version", "fb_launch_count",
 )
 
 
@@ -86,11 +86,12 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
                                             ctypes.c_int32, P(FbStats)]
         lib.fb_spatial_filter.argtypes = [vp, P(FbImage), P(FbImage), P(FbSpatial), ctypes.c_int32, P(FbStats)]
         lib.fb_validate.argtypes = [vp, P(FbImage), ctypes.c_double, ctypes.c_double, P(FbStats)]
+        lib.fb_bilateral_exact.argtypes = [vp, P(FbImage), P(FbImage), P(FbSpatial), ctypes.c_double, P(FbStats)]
         lib.fb_last_error.restype = ctypes.c_char_p
         lib.fb_version.restype = ctypes.c_int
         lib.fb_launch_count.restype = ctypes.c_int64
         for name in ("fb_create", "fb_destroy", "fb_set_stream", "fb_set_workspace_limit", "fb_gpa_filter",
-                     "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate"):
+                     "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate", "fb_bilateral_exact"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
         return lib
@@ -219,6 +220,18 @@ def spatial(src, out, kernel, precision: int, device: int = 0) -> dict:
     st = FbStats()
     rc = lib.fb_spatial_filter(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)), ctypes.byref(sp),
                                int(precision), ctypes.byref(st))
+    _check(lib, rc, src, st)
+    return st.as_dict()
+
+
+def bilateral_exact(src, out, kernel, sigma_r: float, device: int = 0) -> dict:
+    lib = load_library()
+    ctx = context(device)
+    lib.fb_set_stream(ctx, _stream_for(src, device))
+    sp, _taps = spatial_desc(kernel)
+    st = FbStats()
+    rc = lib.fb_bilateral_exact(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)), ctypes.byref(sp),
+                                float(sigma_r), ctypes.byref(st))
     _check(lib, rc, src, st)
     return st.as_dict()
 

@@ -572,6 +572,44 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
   return status;
 }
 
+
+// ---------------------------------------------------------------------------- brute force
+// Exact bilateral filter, O(W^2) per pixel, fp64, replicate boundary: the reference's
+// bilateral_exact (reference.py:17-45), used to report the GPA approximation error at full size.
+// CTA = 16x16 outputs; the (16+2W)^2 input tile (clamped rows/columns) is staged in shared memory.
+constexpr int BF_T = 16;
+
+__global__ void __launch_bounds__(BF_T * BF_T) k_bilateral_exact(const void* f, long long f_ld, int f_dtype,
+                                                                 int rows, int cols, int W, const double* w1d,
+                                                                 double inv_two_sr2, double* out, long long out_ld) {
+  extern __shared__ double bf_tile[];
+  const int S = BF_T + 2 * W;
+  const int y0 = blockIdx.y * BF_T, x0 = blockIdx.x * BF_T;
+  for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
+    const int ty = i / S, tx = i - ty * S;
+    const int gy = min(max(y0 + ty - W, 0), rows - 1), gx = min(max(x0 + tx - W, 0), cols - 1);
+    bf_tile[i] = load_sample(f, f_dtype, (long long)gy * f_ld + gx);
+  }
+  __syncthreads();
+  const int ty = threadIdx.x / BF_T, tx = threadIdx.x % BF_T;
+  const int y = y0 + ty, x = x0 + tx;
+  if (y >= rows || x >= cols) return;
+  const double fi = bf_tile[(ty + W) * S + tx + W];
+  double num = 0.0, den = 0.0;
+  for (int dy = 0; dy <= 2 * W; ++dy) {
+    const double wy = w1d[dy];
+    const double* rowp = bf_tile + (ty + dy) * S + tx;
+    for (int dx = 0; dx <= 2 * W; ++dx) {
+      const double nb = rowp[dx];
+      const double d = nb - fi;
+      const double wgt = wy * w1d[dx] * exp(-d * d * inv_two_sr2);
+      num = fma(wgt, nb, num);
+      den += wgt;
+    }
+  }
+  out[(long long)y * out_ld + x] = num / den;
+}
+
 }  // namespace
 
 extern "C" {
@@ -746,6 +784,79 @@ int fb_validate(fb_ctx* ctx, const fb_image* in, double lo, double hi, fb_stats*
   j.lo = lo;
   j.hi = hi;
   return execute(ctx, in, nullptr, 1, 0, 0, j, FB_PREC_F64, stats);
+}
+
+int fb_bilateral_exact(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_spatial* sp, double sigma_r,
+                       fb_stats* stats) {
+  if (!ctx) return fail(FB_ERR_PARAM, "null context");
+  int rc = check_image(in, "input", true);
+  if (rc) return rc;
+  rc = check_image(out, "output", false);
+  if (rc) return rc;
+  if (!sp || (sp->kind != FB_BOX && sp->kind != FB_GAUSSIAN) || sp->half_width < 1 || sp->half_width > kMaxW ||
+      (sp->kind == FB_GAUSSIAN && !sp->weights_1d))
+    return fail(FB_ERR_PARAM, "bad spatial kernel");
+  if (out->dtype != FB_F64 || out->rows != in->rows || out->cols != in->cols)
+    return fail(FB_ERR_PARAM, "output must be float64 of the input's shape");
+  if (!(sigma_r > 0)) return fail(FB_ERR_PARAM, "sigma_r must be positive");
+  if (sp->half_width >= std::min(in->rows, in->cols))
+    return fail(FB_ERR_WINDOW, "window half-width " + std::to_string(sp->half_width) + " too large for " +
+                                   std::to_string(in->rows) + "x" + std::to_string(in->cols) + " image");
+  FB_CUDA(cudaSetDevice(ctx->device));
+  const int W = sp->half_width, n = 2 * W + 1;
+  std::vector<double> w(n);
+  for (int k = 0; k < n; ++k) w[k] = sp->kind == FB_BOX ? 1.0 / n : sp->weights_1d[k];
+  const size_t ies = dtype_size(in->dtype);
+  fb_stats local;
+  memset(&local, 0, sizeof(local));
+  local.bad_image = -1;
+  void* din = in->data;
+  long long dld = in->ld;
+  void* dout = out->data;
+  long long old = out->ld;
+  double* dw = nullptr;
+  FB_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
+  FB_CUDA(cudaMallocAsync(&dw, n * sizeof(double), ctx->stream));
+  FB_CUDA(cudaMemcpyAsync(dw, w.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  if (!in->on_device) {
+    rc = grow(&ctx->in_stage[0], &ctx->in_stage_bytes[0], (size_t)in->rows * in->cols * ies);
+    if (rc) return rc;
+    FB_CUDA(cudaMemcpy2DAsync(ctx->in_stage[0], in->cols * ies, in->data, in->ld * ies, in->cols * ies, in->rows,
+                              cudaMemcpyHostToDevice, ctx->stream));
+    din = ctx->in_stage[0];
+    dld = in->cols;
+  }
+  if (!out->on_device) {
+    rc = grow(&ctx->out_stage[0], &ctx->out_stage_bytes[0], (size_t)out->rows * out->cols * 8);
+    if (rc) return rc;
+    dout = ctx->out_stage[0];
+    old = out->cols;
+  }
+  const size_t smem = (size_t)(BF_T + 2 * W) * (BF_T + 2 * W) * sizeof(double);
+  FB_CUDA(cudaFuncSetAttribute(k_bilateral_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid((unsigned)((in->cols + BF_T - 1) / BF_T), (unsigned)((in->rows + BF_T - 1) / BF_T));
+  FB_CUDA(cudaEventRecord(ctx->ev_kstart, ctx->stream));
+  k_bilateral_exact<<<grid, BF_T * BF_T, smem, ctx->stream>>>(din, dld, in->dtype, (int)in->rows, (int)in->cols, W,
+                                                                dw, 1.0 / (2.0 * sigma_r * sigma_r),
+                                                                static_cast<double*>(dout), old);
+  FB_CUDA(cudaGetLastError());
+  g_launches += 1;
+  FB_CUDA(cudaEventRecord(ctx->ev_kend, ctx->stream));
+  if (!out->on_device)
+    FB_CUDA(cudaMemcpy2DAsync(out->data, out->ld * 8, dout, old * 8, out->cols * 8, out->rows,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+  FB_CUDA(cudaFreeAsync(dw, ctx->stream));
+  FB_CUDA(cudaEventRecord(ctx->ev_end, ctx->stream));
+  FB_CUDA(cudaEventSynchronize(ctx->ev_end));
+  float ms = 0.f, kms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_end);
+  cudaEventElapsedTime(&kms, ctx->ev_kstart, ctx->ev_kend);
+  local.device_ms = ms;
+  local.kernel_ms = kms;
+  local.launches = 1;
+  local.precision = FB_PREC_F64;
+  if (stats) *stats = local;
+  return FB_OK;
 }
 
 }  // extern "C"

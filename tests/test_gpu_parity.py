@@ -65,6 +65,30 @@ def test_reference_config_crops(name, precision, golden, golden_scalars):
     assert err <= (F64_TOL if precision == "f64" else F32_TOL), err
 
 
+@pytest.mark.parametrize("tag", ["c0", "c1", "c2", "c3", "c4", "impulse3", "random64_gauss5", "ragged_box4",
+                                 "ragged_gauss25", "shift0_gauss2"])
+def test_bilateral_exact_matches_reference(tag, golden, golden_scalars):
+    """GPU brute force (fp64) = the reference's bilateral_exact (reference.py:17-45) outputs."""
+    from paper_1603_08109_b200 import bilateral_exact
+    c = golden_scalars["cases"][tag]
+    if "half_width" in c:
+        k = kern(c["kind"], c["half_width"] if c["kind"] == "box" else c["sigma_s"])
+    else:
+        k = kern(c["kind"], c["param"])
+    out = bilateral_exact(golden[f"{tag}_in"], k, c["sigma_r"])
+    assert np.max(np.abs(out - golden[f"{tag}_exact"])) <= 1e-10
+
+
+def test_bilateral_exact_errors():
+    from paper_1603_08109_b200 import bilateral_exact
+    k = make_spatial_kernel("box", half_width=1)
+    img = np.floor(np.random.default_rng(2).uniform(0, 256, (8, 8)))
+    with pytest.raises(ParameterError):
+        bilateral_exact(img, k, -1.0)
+    with pytest.raises(ParameterError):
+        bilateral_exact(img, make_spatial_kernel("box", half_width=8), 30.0)
+
+
 def test_spatial_filters_match_reference(golden):
     img = golden["spatial_in"]
     for W in (1, 2, 7, 10):

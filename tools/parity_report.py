@@ -23,7 +23,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 from oracle import gpa_oracle as orc  # noqa: E402  (checker only)
-from paper_1603_08109_b200 import gpa_filter, synth  # noqa: E402
+from paper_1603_08109_b200 import bilateral_exact, gpa_filter, synth  # noqa: E402
+
+
+def psnr(mse):
+    """20 log10(255) - mse_db (analysis.py:41-46)."""
+    import math
+    return math.inf if mse == 0 else 20 * math.log10(255.0) - 10 * math.log10(mse)
 
 
 def window_errs(img, out, k, sigma_r, N, windows):
@@ -52,11 +58,19 @@ def main():
         N = synth.config_order(cfg)
         n_img = min(cfg.batch, args.c3_images) if cfg.batch > 1 else 1
         worst, worst_at, q9999, over1e4, npx = 0.0, None, [], 0, 0
+        approx = {"ours_linf": 0.0, "ref_linf": 0.0, "ours_se": 0.0, "ref_se": 0.0}
         t0 = time.time()
         for i in range(n_img):
             img = synth.config_image(cfg, i)
             o32 = gpa_filter(img, k, cfg.sigma_r, N, precision="f32")
             o64 = gpa_filter(img, k, cfg.sigma_r, N, precision="f64")
+            bf = bilateral_exact(img, k, cfg.sigma_r)  # GPU fp64 brute force
+            e32, e64 = np.abs(o32 - bf), np.abs(o64 - bf)
+            approx["ours_linf"] = max(approx["ours_linf"], float(e32.max()))
+            approx["ref_linf"] = max(approx["ref_linf"], float(e64.max()))
+            approx["ours_se"] += float(np.sum(e32 * e32))
+            approx["ref_se"] += float(np.sum(e64 * e64))
+            del bf, e32, e64
             d = np.abs(o32 - o64)
             j = np.unravel_index(int(np.argmax(d)), d.shape)
             if d[j] > worst:
@@ -79,6 +93,10 @@ def main():
             "p99.99_abs": max(q9999), "pixels_over_1e-4": over1e4,
             "windows_max_abs_f32_vs_oracle": w32, "windows_max_abs_f64_vs_oracle": w64,
             "seconds": round(time.time() - t0, 1),
+            # approximation error vs the exact bilateral filter (GPU fp64 brute force): ours (fp32
+            # path) and the reference-equivalent fp64 path (= the reference's gpa_filter to 1e-13)
+            "approx_linf_ours": approx["ours_linf"], "approx_linf_reference": approx["ref_linf"],
+            "approx_psnr_ours": psnr(approx["ours_se"] / npx), "approx_psnr_reference": psnr(approx["ref_se"] / npx),
         }
         print(name, json.dumps(report["configs"][name]), flush=True)
     out = os.path.join(ROOT, "profiles", f"parity_{args.tag}.json")
