@@ -197,13 +197,11 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
       a.wq[2 * q + 1] = q > 0 ? (float)a.w[q - 1] : 0.f;
     }
   }
-  double a32 = 1.0;
-  for (int m = 0; m < kWalkMaxCh; ++m) {
-    const float r = m > 0 ? (float)(1.0 / std::sqrt((double)m)) : 0.f;
-    a.rsc2[2 * m] = a.rsc2[2 * m + 1] = r;
-    if (m >= 1 && m <= 32) a32 *= (double)r;
-  }
-  a.walk_a32 = (float)a32;
+  // Box walker multipliers: it steps each channel parity by two orders at once,
+  // c_n = c_{n-2} * x^2 * q_n with q_n = fl32(1/sqrt((n-1) n)) (q_1 = 1: c_1 = c_0 x), so the
+  // even and odd chains are independent.  Stored as (q_n, q_n) pairs for packed multiplies.
+  for (int m = 0; m < kWalkMaxCh; ++m)
+    a.rsc2[2 * m] = a.rsc2[2 * m + 1] = walk_q(m);
   // channel constants 1/sqrt(m), sqrt(m) (rounded once from double), uploaded when N changes
   if (j.N + 1 > ctx->tab_cap) {
     for (void* p : {(void*)ctx->tab, (void*)ctx->tabd}) if (p) cudaFree(p);
@@ -217,8 +215,8 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
     const int cap = std::max(j.N + 1, 256);
     FB_CUDA(cudaMalloc(&ctx->tab, 4 * sizeof(float) * cap));
     FB_CUDA(cudaMallocHost(&ctx->tab_host, 4 * sizeof(float) * cap));
-    FB_CUDA(cudaMalloc(&ctx->tabd, 2 * sizeof(double) * cap));
-    FB_CUDA(cudaMallocHost(&ctx->tabd_host, 2 * sizeof(double) * cap));
+    FB_CUDA(cudaMalloc(&ctx->tabd, 4 * sizeof(double) * cap));  // [sequential | walker] sections
+    FB_CUDA(cudaMallocHost(&ctx->tabd_host, 4 * sizeof(double) * cap));
     ctx->tab_cap = cap;
   }
   if (ctx->tab_n != j.N) {
@@ -236,14 +234,32 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
       ctx->tabd_host[2 * m] = h;
       ctx->tabd_host[2 * m + 1] = sg;
     }
+    // The same constants for planes made by the box walker: its channel m carries the
+    // normalisation A_m = q_m A_{m-2} (A_0 = A_1 = 1), i.e. an effective r'_m = A_m / A_{m-1}.
+    double* wd = ctx->tabd_host + 2 * ctx->tab_cap;
+    double A2 = 1.0, A1 = 1.0;  // A_{m-2}, A_{m-1}
+    for (int m = 0; m <= j.N; ++m) {
+      double h = 0.0, sg = 0.0;
+      if (m >= 1 && m < kWalkMaxCh) {
+        const double Am = m == 1 ? 1.0 : (double)walk_q(m) * A2;
+        const double r = Am / A1;
+        h = 1.0 / ((double)m * r);
+        sg = 1.0 / r;
+        A2 = A1;
+        A1 = Am;
+      }
+      wd[2 * m] = h;
+      wd[2 * m + 1] = sg;
+    }
     FB_CUDA(cudaMemcpyAsync(ctx->tab, ctx->tab_host, 4 * sizeof(float) * (j.N + 1), cudaMemcpyHostToDevice,
                             ctx->stream));
-    FB_CUDA(cudaMemcpyAsync(ctx->tabd, ctx->tabd_host, 2 * sizeof(double) * (j.N + 1), cudaMemcpyHostToDevice,
+    FB_CUDA(cudaMemcpyAsync(ctx->tabd, ctx->tabd_host, 4 * sizeof(double) * ctx->tab_cap, cudaMemcpyHostToDevice,
                             ctx->stream));
     ctx->tab_n = j.N;
   }
   a.tab = ctx->tab;
-  a.tabd = ctx->tabd;
+  a.tabd = a.tabd_seq = ctx->tabd;
+  a.tabd_walk = ctx->tabd + 2 * ctx->tab_cap;
   a.wpad = cols + 2 * j.W;
   a.pitch = (a.wpad + 31) / 32 * 32;
   // Row bands: the N+1 planes of one band must fit under the workspace limit.

@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
+
 namespace fbgpu {
 
 constexpr int kMaxW = 160;                  // largest half-width the kernels accept
@@ -62,20 +64,28 @@ struct GpaArgs {
   // fp32 channel constants, 4 per channel m: r_m = fl32(1/sqrt(m)) (0 for m = 0), sqrt(m),
   // and the matched Horner constants h_m = 1/(m r_m), s_m = 1/r_m rounded to fp32
   const float* tab;
-  // fp64 Horner constants matched to r_m (see k2f_hpass_horner): tabd[2m] = 1/(m r_m), tabd[2m+1] = 1/r_m
+  // fp64 Horner constants matched to r_m (see k2f_hpass_horner): tabd[2m] = 1/(m r_m), tabd[2m+1] = 1/r_m.
+  // tabd is the set matching the kernel that made the planes: tabd_seq (c_m = c_{m-1} x r_m) or
+  // tabd_walk (the box walker's two-step recurrence, r_m replaced by its effective ratio).
   const double* tabd;
+  const double* tabd_seq;
+  const double* tabd_walk;
   T w[kMaxTaps];      // normalised 1-D taps (gaussian)
   // Tap pairs for packed FFMA2 (fp32 fast path): wq[2a] = w[a], wq[2a+1] = w[a-1],
   // a = 0 .. 2W+1, with w[-1] = w[2W+1] = 0 (box: all ones).
   alignas(8) float wq[2 * (2 * kFastMaxW + 2)];
-  // (1/sqrt(n), 1/sqrt(n)) pairs for n < kWalkMaxCh, compile-time-indexed by the box walker
+  // (q_n, q_n) pairs for n < kWalkMaxCh: the box walker's two-step multipliers (walk_q)
   alignas(8) float rsc2[2 * 64];
   int walk_rows;      // output rows per thread of the box walker
-  float walk_a32;     // prod_{k=1..32} r_k (start of the second channel half of the box walker)
   int n_delta1;       // order Algorithm 1 picks for delta = 1 gray level (Horner-precision policy)
 };
 
 constexpr int kWalkMaxCh = 64;              // channels (N+1) the register-resident box walker holds
+
+// Box walker multiplier q_n: c_n = c_{n-2} x^2 q_n, q_1 = 1 (c_1 = c_0 x), q_n = fl32(1/sqrt((n-1) n)).
+__host__ __device__ inline float walk_q(int n) {
+  return n <= 0 ? 0.f : (n == 1 ? 1.f : (float)(1.0 / sqrt((double)(n - 1) * (double)n)));
+}
 
 __device__ __forceinline__ double load_sample(const void* f, int dt, long long idx) {
   if (dt == 1) return (double)__ldg(reinterpret_cast<const float*>(f) + idx);
