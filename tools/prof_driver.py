@@ -18,7 +18,10 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--rows", type=int, default=0, help="crop rows (0 = full image)")
+ap.add_argument("--lib", default=None, help="alternative libfbgpu.so (A/B experiments)")
 args = ap.parse_args()
+if args.lib:
+    _native.load_library(args.lib)
 cfg = synth.CONFIGS[args.config]
 img = synth.config_image(cfg)
 if args.rows:
@@ -30,4 +33,4 @@ out = torch.empty(img.shape, dtype=torch.float32, device="cuda")
 for _ in range(args.reps):
     st = _native.gpa(d, out, k, cfg.sigma_r, N, 128.0, 128.0, _native.FB_PREC_F32, 0)
 torch.cuda.synchronize()
-print(f"{args.config} {img.shape} N={N} k1_ms={st['k1_ms']:.3f} k2_ms={st['k2_ms']:.3f} bands={st['bands']}")
+print(f"{args.lib or ''} {args.config} {img.shape} N={N} k1_ms={st['k1_ms']:.3f} k2_ms={st['k2_ms']:.3f} bands={st['bands']}")
