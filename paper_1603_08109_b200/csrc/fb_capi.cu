@@ -336,6 +336,9 @@ struct Item {
 
 // Copy-in / filter / copy-out for `count` images.  Host-resident images are pipelined in
 // row chunks over three streams: H2D of chunk c+1 || kernels of chunk c || D2H of chunk c-1.
+#ifndef FB_CHUNK_PX
+#define FB_CHUNK_PX (8ll << 20)
+#endif
 // Kernels of a chunk wait for the input rows they read (chunk rows + W halo rows).
 template <typename T>
 int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bottom, const Job& j,
@@ -515,10 +518,14 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
     it.out = outs ? outs + i : nullptr;
     it.rows_out = (int)(ins[i].rows - halo_top - halo_bottom);
     pixels += (long long)it.rows_out * ins[i].cols;
-    // host images of more than 4 MP are pipelined in 8 row chunks
+    // host images of more than 4 MP are pipelined in row chunks of ~FB_CHUNK_PX pixels (at least
+    // 8 chunks, at most 64, >= 256 rows each): the un-overlapped first H2D and last D2H shrink
+    // with the chunk, while per-chunk launches and events stay negligible
     const bool host_io = !ins[i].on_device || (it.out && !it.out->on_device);
     const long long px = (long long)it.rows_out * ins[i].cols;
-    it.chunks = (host_io && px >= (4ll << 20) && it.rows_out >= 512) ? 8 : 1;
+    long long nch = std::min<long long>(64, std::max<long long>(8, px / FB_CHUNK_PX));
+    nch = std::max<long long>(1, std::min<long long>(nch, it.rows_out / 256));
+    it.chunks = (host_io && px >= (4ll << 20) && it.rows_out >= 512) ? (int)nch : 1;
   }
   const long long launches0 = g_launches.load();
   FB_CUDA(cudaEventRecord(ctx->ev_kstart, ctx->stream));
