@@ -1,0 +1,115 @@
+"""GPU parity of the large-image box path (kernel 1 = the column walker with TMA row stores,
+kernel 2 = the fast horizontal pass + fp64 Horner) and of kernel 2's epilogue paths.
+
+The walker runs when (cols + 2W) x band_rows >= 4 Mi samples and N+1 <= 64, so these images are
+~2100^2.  Full images are compared with the fp64 path (pinned to the reference at 1e-9 by
+test_gpu_parity.py); windows are compared with the oracle itself.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import gpa_oracle as orc
+from paper_1603_08109_b200 import _native, gpa_filter, make_spatial_kernel, synth
+
+pytestmark = pytest.mark.gpu
+
+F32_TOL = 1e-3
+SIDE = 2100  # (2100 + 2W) * 2100 >= 4 Mi: walker territory
+
+
+def _windows(H, Wd):
+    return [(0, 0, 40, 40), (H - 40, Wd - 40, 40, 40), (H // 2 + 3, Wd // 3 + 5, 48, 48), (0, Wd - 40, 40, 40)]
+
+
+def _oracle_windows(img, out, k, sigma_r, N):
+    W = k.half_width
+    H, Wd = img.shape
+    worst = 0.0
+    for (y, x, h, w) in _windows(H, Wd):
+        y0, x0 = max(0, y - W), max(0, x - W)
+        y1, x1 = min(H, y + h + W), min(Wd, x + w + W)
+        sub = orc.gpa(img[y0:y1, x0:x1].astype(np.float64), "box", W, k.weights_1d, sigma_r, N)
+        ref = sub[y - y0:y - y0 + h, x - x0:x - x0 + w]
+        worst = max(worst, float(np.max(np.abs(out[y:y + h, x:x + w] - ref))))
+    return worst
+
+
+# Orders are in the convergent regime of each sigma_r (Algorithm 1 at delta = 1 gives >= these;
+# N = 7 at sigma_r = 400 covers the smallest channel capacity, which Algorithm 1's floor of 10
+# never selects).  Far below Algorithm 1's order the truncated series itself is meaningless
+# (outputs of 1e6 gray levels) and no fp32 bar applies.
+@pytest.mark.parametrize("W,N,sigma_r,dtype", [
+    (1, 7, 400.0, np.float32),    # NCH 8
+    (1, 49, 25.0, np.float32),    # smallest window at its Algorithm-1 order (delta = 1)
+    (5, 10, 150.0, np.float32),   # NCH 16, N+1 just past a multiple of 8
+    (3, 28, 40.0, np.uint8),      # register-path input (no cp.async ring)
+    (20, 57, 25.0, np.float32),   # c4's filter
+    (20, 57, 25.0, np.float64),
+    (32, 63, 23.5, np.float32),   # NCH 64 = the walker's capacity, widest fast window
+])
+def test_walker_matches_oracle_and_fp64(W, N, sigma_r, dtype):
+    img = synth.config_image("c4", height=SIDE, width=SIDE)  # c4 recipe: outliers included
+    img = np.floor(img).astype(dtype)
+    k = make_spatial_kernel("box", half_width=W)
+    out = gpa_filter(img, k, sigma_r, N, precision="f32")
+    ref64 = gpa_filter(img, k, sigma_r, N, precision="f64")
+    assert np.max(np.abs(out - ref64)) <= 5e-4
+    assert _oracle_windows(img, out, k, sigma_r, N) <= F32_TOL
+
+
+def test_walker_band_partitions_agree():
+    """Several walker bands (workspace limit) and an explicit halo-band call agree with one band."""
+    torch = pytest.importorskip("torch")
+    img = synth.config_image("c4", height=4096, width=2048)
+    k = make_spatial_kernel("box", half_width=20)
+    N = 57
+    one, many = {}, {}
+    dimg = torch.from_numpy(img).cuda()  # device-resident: no host row chunks
+    full = gpa_filter(dimg, k, 25.0, N, precision="f32", stats=one).cpu().numpy()
+    pitch = (2048 + 40 + 31) // 32 * 32
+    _native.set_workspace_limit(2048 * (N + 1) * pitch * 4)  # two bands of 2048 rows
+    try:
+        banded = gpa_filter(dimg, k, 25.0, N, precision="f32", stats=many).cpu().numpy()
+    finally:
+        _native.set_workspace_limit(8 << 30)
+    assert one["bands"] == 1 and many["bands"] == 2
+    ref64 = gpa_filter(img, k, 25.0, N, precision="f64")
+    assert np.max(np.abs(full - ref64)) <= 5e-4
+    assert np.max(np.abs(banded - ref64)) <= 5e-4
+    # rows [1000, 3100) from a buffer holding only those rows plus W halo rows each side
+    r0, r1, W = 1000, 3100, 20
+    ext = torch.from_numpy(np.ascontiguousarray(img[r0 - W:r1 + W])).cuda()
+    out = torch.empty((r1 - r0, img.shape[1]), dtype=torch.float32, device="cuda")
+    _native.gpa(ext, out, k, 25.0, N, 128.0, 128.0, _native.FB_PREC_F32, 0, halo_top=W, halo_bottom=W)
+    assert np.max(np.abs(out.cpu().numpy() - ref64[r0:r1])) <= 5e-4
+
+
+@pytest.mark.parametrize("width", [128, 130, 131, 133, 1029])
+def test_fp32_output_vector_and_scalar_stores(width):
+    """float32 outputs use 128-bit stores where the row segment is aligned and complete, scalar
+    stores elsewhere (odd widths, ragged right edge): both must hold the same values."""
+    rng = np.random.default_rng(width)
+    img = np.floor(rng.uniform(0.0, 256.0, (70, width)))
+    for k, N in ((make_spatial_kernel("box", half_width=5), 20), (make_spatial_kernel("gaussian", sigma_s=3.0), 15)):
+        o32 = gpa_filter(img, k, 30.0, N, precision="f32", out_dtype=np.float32)
+        o64 = gpa_filter(img, k, 30.0, N, precision="f32")
+        assert o32.dtype == np.float32
+        assert np.array_equal(o32, o64.astype(np.float32))
+        ref = orc.gpa(img, k.kind, k.half_width, k.weights_1d, 30.0, N)
+        assert np.max(np.abs(o64 - ref)) <= F32_TOL
+
+
+def test_fast_path_q_floor_passthrough(golden):
+    """The fp32 kernels' epilogue applies the reference's |Q| < 1e-30 pass-through
+    (engine.py:20, 68) like the fp64 path: same pixels, same values."""
+    img = np.zeros((5, 5))
+    img[2, 2] = 255.0
+    k = make_spatial_kernel("box", half_width=1)
+    s32, s64 = {}, {}
+    o32 = gpa_filter(img, k, 10.0, 1, allow_small_sigma=True, precision="f32", stats=s32)
+    o64 = gpa_filter(img, k, 10.0, 1, allow_small_sigma=True, precision="f64", stats=s64)
+    assert s64["degenerate_pixels"] > 0
+    assert s32["degenerate_pixels"] == s64["degenerate_pixels"]
+    assert np.max(np.abs(o32 - golden["qdegenerate5_out"])) <= F32_TOL
+    assert np.max(np.abs(o64 - golden["qdegenerate5_out"])) <= 1e-9
