@@ -525,7 +525,8 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
     const long long px = (long long)it.rows_out * ins[i].cols;
     long long nch = std::min<long long>(64, std::max<long long>(8, px / FB_CHUNK_PX));
     nch = std::max<long long>(1, std::min<long long>(nch, it.rows_out / 256));
-    it.chunks = (host_io && px >= (4ll << 20) && it.rows_out >= 512) ? (int)nch : 1;
+    // (batches overlap image i+1's copies with image i's kernels instead: no chunks)
+    it.chunks = (count == 1 && host_io && px >= (4ll << 20) && it.rows_out >= 512) ? (int)nch : 1;
   }
   const long long launches0 = g_launches.load();
   FB_CUDA(cudaEventRecord(ctx->ev_kstart, ctx->stream));

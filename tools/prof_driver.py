@@ -32,15 +32,20 @@ N = synth.config_order(cfg)
 if args.e2e:
     import time
 
-    from paper_1603_08109_b200 import gpa_filter
-    pin = torch.from_numpy(img).pin_memory().numpy()
-    pout = torch.empty(img.shape, dtype=torch.float64).pin_memory().numpy()
+    from paper_1603_08109_b200 import gpa_filter, gpa_filter_batch
+    imgs = [img] + [synth.config_image(cfg, i) for i in range(1, cfg.batch)]
+    pin = [torch.from_numpy(im).pin_memory().numpy() for im in imgs]
+    pout = [torch.empty(im.shape, dtype=torch.float64).pin_memory().numpy() for im in imgs]
     best = 1e9
     for _ in range(args.reps + 1):
         t0 = time.perf_counter()
-        gpa_filter(pin, k, cfg.sigma_r, N, precision="f32", device=0, out=pout)
+        if len(pin) > 1:
+            gpa_filter_batch(pin, k, cfg.sigma_r, N, precision="f32", device=0, outs=pout)
+        else:
+            gpa_filter(pin[0], k, cfg.sigma_r, N, precision="f32", device=0, out=pout[0])
         best = min(best, time.perf_counter() - t0)
-    print(f"{args.lib or ''} {args.config} e2e {best * 1e3:.2f} ms = {img.size / best / 1e6:.0f} MP/s")
+    px = sum(im.size for im in imgs)
+    print(f"{args.lib or ''} {args.config} e2e {best * 1e3:.2f} ms = {px / best / 1e6:.0f} MP/s")
     sys.exit(0)
 d = torch.from_numpy(img).cuda()
 out = torch.empty(img.shape, dtype=torch.float32, device="cuda")
