@@ -277,8 +277,13 @@ def main():
     dev_out = [torch.empty(im.shape, dtype=torch.float32, device=dev) for im in host_imgs]
     my_pixels = sum(im.shape[0] * im.shape[1] for im in host_imgs)
     root_full = None
-    if bands is not None and rank == 0:
-        root_full = torch.empty((cfg.height, cfg.width), dtype=torch.float32, device=dev)
+    peer = None
+    if bands is not None:
+        # the final gather is fused into kernel 2: every rank writes its rows straight into the
+        # root's buffer over NVLink / NVSwitch (sharding.PeerOutput, CUDA IPC)
+        if rank == 0:
+            root_full = torch.empty((cfg.height, cfg.width), dtype=torch.float32, device=dev)
+        peer = sharding.PeerOutput(root_full, (cfg.height, cfg.width), torch.float32, rank, local)
     flush = None
     if cfg.pixels * 4 <= 126e6:
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -290,10 +295,11 @@ def main():
         if bands is not None:
             ext = sharding.exchange_halos(dev_imgs[0], W, rank, world, bands)
             top, bottom = bands.halos(rank)
-            st = _native.gpa(ext, dev_out[0], kernel, cfg.sigma_r, N, 128.0, 128.0, _native.FB_PREC_F32, local,
-                             halo_top=top, halo_bottom=bottom)
+            r0, r1 = bands.bounds(rank)
+            st = _native.gpa(ext, peer.band(r0, r1), kernel, cfg.sigma_r, N, 128.0, 128.0, _native.FB_PREC_F32,
+                             local, halo_top=top, halo_bottom=bottom)
             sts = [st]
-            sharding.gather_rows(dev_out[0], root_full, rank, world, bands)
+            peer.done()
         elif len(dev_imgs) > 1:
             sts = [_native.gpa_batch(dev_imgs, dev_out, kernel, cfg.sigma_r, N, 128.0, 128.0,
                                      _native.FB_PREC_F32, local)]
@@ -372,6 +378,9 @@ def main():
                + ("; at N>1 each rank filters its own band (halo rows replicated at band edges in this leg)"
                   if bands is not None else "")}
 
+    if peer is not None:
+        dist.barrier()  # every rank is done writing into the root's buffer before unmapping
+        peer.close()
     if rank != 0:
         if world > 1:
             dist.barrier()

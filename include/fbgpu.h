@@ -161,6 +161,23 @@ int fb_validate(fb_ctx* ctx, const fb_image* in, double lo, double hi, fb_stats*
 int fb_bilateral_exact(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_spatial* spatial,
                        double sigma_r, fb_stats* stats);
 
+/*
+ * Peer output buffers for the row-band partitioning (north star item 5: "no collective beyond a
+ * final gather").  The root exports its full-image output allocation; every other rank maps it
+ * and passes a row slice of it as `out` to fb_gpa_filter, so kernel 2's epilogue stores the
+ * band straight into the root's HBM over NVLink / NVSwitch: the gather is fused into the
+ * filter and needs no receive buffers or separate collective.  Replaces the reference's
+ * single-process output assembly (the whole image is filtered in one call there, engine.py:27).
+ *   fb_ipc_export: handle (64 bytes) of the allocation holding dptr, *offset = dptr - base.
+ *   fb_ipc_open:   map a peer's handle on `device`; *base = mapping, caller adds the offset.
+ *   fb_ipc_close:  unmap a base returned by fb_ipc_open.
+ * Writers must finish (the filter call returns synchronously) and signal the root (e.g. a
+ * barrier) before the root reads the rows.
+ */
+int fb_ipc_export(const void* dptr, uint8_t handle[64], int64_t* offset);
+int fb_ipc_open(int32_t device, const uint8_t handle[64], void** base);
+int fb_ipc_close(void* base);
+
 /* Message of the last failure on this host thread. */
 const char* fb_last_error(void);
 int fb_version(void);

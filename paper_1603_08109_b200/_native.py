@@ -29,7 +29,7 @@ FB_PREC_F32, FB_PREC_F64 = 1, 2
 EXPORTED_SYMBOLS = (
     "fb_create", "fb_destroy", "fb_set_stream", "fb_set_workspace_limit", "fb_gpa_filter",
     "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate", "fb_bilateral_exact", "fb_last_error",
-    "fb_version", "fb_launch_count",
+    "fb_version", "fb_launch_count", "fb_ipc_export", "fb_ipc_open", "fb_ipc_close",
 )
 
 
@@ -77,6 +77,9 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         lib.fb_create.argtypes = [ctypes.c_int, P(vp)]
         lib.fb_destroy.argtypes = [vp]
         lib.fb_set_stream.argtypes = [vp, vp]
+        lib.fb_ipc_export.argtypes = [vp, ctypes.c_char_p, P(ctypes.c_int64)]
+        lib.fb_ipc_open.argtypes = [ctypes.c_int32, ctypes.c_char_p, P(vp)]
+        lib.fb_ipc_close.argtypes = [vp]
         lib.fb_set_workspace_limit.argtypes = [vp, ctypes.c_int64]
         lib.fb_gpa_filter.argtypes = [vp, P(FbImage), ctypes.c_int64, ctypes.c_int64, P(FbImage), P(FbSpatial),
                                       ctypes.c_double, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
@@ -130,7 +133,10 @@ def is_cuda_tensor(x) -> bool:
 
 
 def image_desc(arr) -> FbImage:
-    """fb_image for a 2-D numpy array (host) or CUDA torch tensor (device); rows must be unit-stride."""
+    """fb_image for a 2-D numpy array (host) or CUDA torch tensor (device); rows must be unit-stride.
+    An FbImage passes through (e.g. a row slice of a peer's buffer, sharding.PeerOutput)."""
+    if isinstance(arr, FbImage):
+        return arr
     if is_cuda_tensor(arr):
         rs, cs = arr.stride()
         if cs != 1:
@@ -140,6 +146,29 @@ def image_desc(arr) -> FbImage:
     if arr.strides[1] != isz or arr.strides[0] % isz or arr.strides[0] < arr.shape[1] * isz:
         raise ValueError("array rows must be contiguous")
     return FbImage(arr.ctypes.data, _NP_DT[arr.dtype], 0, arr.shape[0], arr.shape[1], arr.strides[0] // isz)
+
+
+def ipc_export(dptr: int) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of the allocation holding dptr, offset of dptr in it)."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    _check(lib, lib.fb_ipc_export(ctypes.c_void_p(dptr), buf, ctypes.byref(off)), None, None)
+    return buf.raw, int(off.value)
+
+
+def ipc_open(device: int, handle: bytes) -> int:
+    """Map a peer allocation on `device`; returns its base address in this process."""
+    lib = load_library()
+    base = ctypes.c_void_p(0)
+    _check(lib, lib.fb_ipc_open(int(device), ctypes.create_string_buffer(handle, 64), ctypes.byref(base)),
+           None, None)
+    return int(base.value)
+
+
+def ipc_close(base: int) -> None:
+    lib = load_library()
+    _check(lib, lib.fb_ipc_close(ctypes.c_void_p(base)), None, None)
 
 
 def spatial_desc(kernel):

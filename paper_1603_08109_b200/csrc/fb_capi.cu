@@ -1,5 +1,6 @@
 // fb_capi.cu — the C ABI (include/fbgpu.h): context, workspace, row-band
 // scheduling, kernel dispatch and error reporting.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -637,6 +638,48 @@ __global__ void __launch_bounds__(BF_T * BF_T) k_bilateral_exact(const void* f, 
 }  // namespace
 
 extern "C" {
+
+int fb_ipc_export(const void* dptr, uint8_t handle[64], int64_t* offset) {
+  if (!dptr || !handle || !offset) return fail(FB_ERR_PARAM, "null argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+  // the handle names the whole allocation: report where dptr sits inside it
+  typedef CUresult (*range_fn_t)(CUdeviceptr*, size_t*, CUdeviceptr);
+  static range_fn_t range_fn = nullptr;
+  if (!range_fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return fail(FB_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    range_fn = reinterpret_cast<range_fn_t>(p);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range_fn(&base, &size, reinterpret_cast<CUdeviceptr>(dptr)) != CUDA_SUCCESS)
+    return fail(FB_ERR_PARAM, "pointer is not a device allocation");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) return fail(FB_ERR_CUDA, std::string("cudaIpcGetMemHandle: ") + cudaGetErrorString(e));
+  memcpy(handle, &h, 64);
+  *offset = (int64_t)(reinterpret_cast<CUdeviceptr>(dptr) - base);
+  return FB_OK;
+}
+
+int fb_ipc_open(int32_t device, const uint8_t handle[64], void** base) {
+  if (!handle || !base) return fail(FB_ERR_PARAM, "null argument");
+  FB_CUDA(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) return fail(FB_ERR_CUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+  return FB_OK;
+}
+
+int fb_ipc_close(void* base) {
+  cudaError_t e = cudaIpcCloseMemHandle(base);
+  if (e != cudaSuccess) return fail(FB_ERR_CUDA, std::string("cudaIpcCloseMemHandle: ") + cudaGetErrorString(e));
+  return FB_OK;
+}
 
 int fb_version(void) { return FBGPU_VERSION; }
 int64_t fb_launch_count(void) { return (int64_t)g_launches.load(); }

@@ -9,8 +9,11 @@ Two partitionings, both with no collective on the data path beyond the final gat
   the INPUT from each neighbour (one point-to-point exchange, 2 x W x cols
   samples, `exchange_halos`) and then filters its band with the halo rows
   passed to the C ABI (`fb_gpa_filter(..., halo_top, halo_bottom, ...)`),
-  which replicates only at the true image edges.  The outputs are gathered to
-  the root with point-to-point receives into row slices (`gather_rows`).
+  which replicates only at the true image edges.  The final gather is fused
+  into the filter: the root's output buffer is mapped into every rank
+  (`PeerOutput`, CUDA IPC over NVLink / NVSwitch) and each rank's kernel 2
+  stores its rows straight into it.  `gather_rows` (point-to-point receives
+  into row slices) is the same gather as a separate collective, for gloo/CPU.
 
 Over NCCL the point-to-point ops move device memory peer-to-peer over
 NVLink/NVSwitch; over gloo the same code runs on CPU tensors (tests).
@@ -100,3 +103,60 @@ def gather_rows(out_band, full, rank: int, world: int, bands: RowBands, root: in
         return full
     dist.send(out_band.contiguous(), root, group)
     return None
+
+
+class PeerOutput:
+    """The root's full-image output, writable by every rank (north star item 5's final gather,
+    fused into the filter's epilogue).
+
+    The root exports the CUDA IPC handle of its output allocation (`fb_ipc_export`); the other
+    ranks map it (`fb_ipc_open`) and pass `band(r0, r1)` -- an `FbImage` row slice of the
+    root's buffer -- as the output of `_native.gpa`.  Kernel 2 then writes those rows over
+    NVLink / NVSwitch directly into the root's HBM: no receive buffers, no gather kernel, no
+    NCCL call.  `done()` is the hand-off: each rank's filter call has returned (it synchronises
+    its stream), and a barrier tells the root every band has landed.
+    """
+
+    def __init__(self, full, shape, dtype, rank: int, device: int, root: int = 0, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import _native
+
+        self.rank, self.root, self.group = rank, root, group
+        self.rows, self.cols = shape
+        self.dtype = _native._TORCH_DT[str(dtype)]
+        self.itemsize = torch.empty((), dtype=dtype).element_size()
+        self._base = None
+        payload = [None]
+        if rank == root:
+            if full.stride(1) != 1 or full.stride(0) != self.cols:
+                raise ValueError("root buffer must be a contiguous (rows, cols) tensor")
+            handle, offset = _native.ipc_export(full.data_ptr())
+            payload = [(handle, offset)]
+            self.ptr = full.data_ptr()
+        dist.broadcast_object_list(payload, src=root, group=group)
+        if rank != root:
+            handle, offset = payload[0]
+            self._base = _native.ipc_open(device, handle)
+            self.ptr = self._base + offset
+
+    def band(self, r0: int, r1: int):
+        """fb_image for rows [r0, r1) of the root's buffer (device memory of the root GPU)."""
+        from . import _native
+
+        return _native.FbImage(self.ptr + r0 * self.cols * self.itemsize, self.dtype, 1, r1 - r0, self.cols,
+                               self.cols)
+
+    def done(self):
+        """Barrier after every rank's (synchronous) filter call: the root's rows are complete."""
+        import torch.distributed as dist
+
+        dist.barrier(group=self.group)
+
+    def close(self):
+        from . import _native
+
+        if self._base is not None:
+            _native.ipc_close(self._base)
+            self._base = None
