@@ -340,6 +340,9 @@ struct Item {
 #ifndef FB_CHUNK_PX
 #define FB_CHUNK_PX (8ll << 20)
 #endif
+#ifndef FB_CHUNK_MIN
+#define FB_CHUNK_MIN 8
+#endif
 // Kernels of a chunk wait for the input rows they read (chunk rows + W halo rows).
 template <typename T>
 int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bottom, const Job& j,
@@ -524,7 +527,7 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
     // with the chunk, while per-chunk launches and events stay negligible
     const bool host_io = !ins[i].on_device || (it.out && !it.out->on_device);
     const long long px = (long long)it.rows_out * ins[i].cols;
-    long long nch = std::min<long long>(64, std::max<long long>(8, px / FB_CHUNK_PX));
+    long long nch = std::min<long long>(64, std::max<long long>(FB_CHUNK_MIN, px / FB_CHUNK_PX));
     nch = std::max<long long>(1, std::min<long long>(nch, it.rows_out / 256));
     // (batches overlap image i+1's copies with image i's kernels instead: no chunks)
     it.chunks = (count == 1 && host_io && px >= (4ll << 20) && it.rows_out >= 512) ? (int)nch : 1;
