@@ -194,6 +194,19 @@ def run_cpu(img, cfg, N, rows, cores):
     return time.perf_counter() - t0
 
 
+def host_info() -> dict:
+    """The CPU the baselines ran on (core count, model, thread variables)."""
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            model = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), "")
+    except OSError:
+        pass
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(),
+            "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"),
+            "FASTBILATERAL_THREADS": os.environ.get("FASTBILATERAL_THREADS")}
+
+
 def reference_arm(args, cfg, N):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -217,7 +230,8 @@ def reference_arm(args, cfg, N):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (paper_1603_08109_b200/synth.py, seeded)", "config": config_block(cfg, N, args.gpus),
-        "cpu_baseline": {"value": value, "unit": "MP/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "MP/s", "cores": cores, "kind": "port", "sample": sample,
+                         "host": host_info()},
         "e2e": {"value": value, "unit": "MP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -438,7 +452,8 @@ def main():
         secs = run_cpu(img0, cfg, N, rows, 1)
         cpu = {"value": rows * cols / 1e6 / secs, "unit": "MP/s", "cores": 1, "kind": "port",
                "sample": f"first {rows} rows x {cols} cols of image 0 ({rows * cols / 1e6:.2f} MP), numpy fp64 "
-                         f"restatement of the reference (oracle/gpa_oracle.py), one process"}
+                         f"restatement of the reference (oracle/gpa_oracle.py), one process",
+               "host": host_info()}
 
     line = {
         "metric": METRIC, "value": value, "unit": "MP/s", "n_gpus": world, "steps": args.steps,
