@@ -1,5 +1,6 @@
 """GPU parity of the large-image box path (kernel 1 = the column walker with TMA row stores,
-kernel 2 = the fast horizontal pass + fp64 Horner) and of kernel 2's epilogue paths.
+kernel 2 = the fast horizontal pass + fp64 Horner; and the fp64 walker / kernel 2 of
+fb_fast64.cuh) and of kernel 2's epilogue paths.
 
 The walker runs when (cols + 2W) x band_rows >= 4 Mi samples and N+1 <= 64, so these images are
 ~2100^2.  Full images are compared with the fp64 path (pinned to the reference at 1e-9 by
@@ -56,6 +57,8 @@ def test_walker_matches_oracle_and_fp64(W, N, sigma_r, dtype):
     ref64 = gpa_filter(img, k, sigma_r, N, precision="f64")
     assert np.max(np.abs(out - ref64)) <= 5e-4
     assert _oracle_windows(img, out, k, sigma_r, N) <= F32_TOL
+    # the fp64 path at this size runs its own walker (fb_fast64.cuh): oracle-exact
+    assert _oracle_windows(img, ref64, k, sigma_r, N) <= 1e-8
 
 
 def test_walker_band_partitions_agree():
@@ -113,3 +116,23 @@ def test_fast_path_q_floor_passthrough(golden):
     assert s32["degenerate_pixels"] == s64["degenerate_pixels"]
     assert np.max(np.abs(o32 - golden["qdegenerate5_out"])) <= F32_TOL
     assert np.max(np.abs(o64 - golden["qdegenerate5_out"])) <= 1e-9
+
+
+@pytest.mark.parametrize("kind,param,N", [("gaussian", 5.0, 42), ("gaussian", 8.0, 60), ("box", 20, 57)])
+def test_fp64_fast_kernels_match_oracle_windows(kind, param, N):
+    """precision="f64" on a large image runs the specialised fp64 kernels (fb_fast64.cuh):
+    the reference's fp64 arithmetic to 1e-8 gray levels."""
+    img = synth.config_image("c2", height=1200, width=1100)
+    k = (make_spatial_kernel("box", half_width=int(param)) if kind == "box"
+         else make_spatial_kernel("gaussian", sigma_s=param))
+    sigma_r = 12.0  # below the fp32 floor: the "auto" policy's fp64 regime
+    out = gpa_filter(img, k, sigma_r, N, allow_small_sigma=True)  # auto -> f64
+    W = k.half_width
+    H, Wd = img.shape
+    worst = 0.0
+    for (y, x, h, w) in _windows(H, Wd):
+        y0, x0 = max(0, y - W), max(0, x - W)
+        y1, x1 = min(H, y + h + W), min(Wd, x + w + W)
+        sub = orc.gpa(img[y0:y1, x0:x1].astype(np.float64), kind, W, k.weights_1d, sigma_r, N)
+        worst = max(worst, float(np.max(np.abs(out[y:y + h, x:x + w] - sub[y - y0:y - y0 + h, x - x0:x - x0 + w]))))
+    assert worst <= 1e-8, worst
