@@ -286,7 +286,17 @@ __global__ void __launch_bounds__(KD2_THREADS, 1)
     qd[j] = 0.0;
   }
 
-  auto load_window = [&](int it, double* win) {
+  // Box windows (<= 72 doubles) are copied to registers and the stage released at once; the
+  // Gaussian reads its taps' inputs straight from shared memory (its 8 x (2W+1) DFMAs would not
+  // fit a register window) and releases the stage after the horizontal pass.
+  constexpr bool kSmemWin = KIND == kKindGauss;
+  double win[kSmemWin ? 2 : WIN];
+  const double* wsm = nullptr;
+  auto release = [&](int it) {
+    __syncwarp();
+    mbar_arrive_if(empty + it % STAGES, lane == 0);
+  };
+  auto load_window = [&](int it) {
     const int s = it % STAGES;
     if (threadIdx.x == 0 && it >= 1 && it - 1 + STAGES <= N) {
       const int sp = (it - 1) % STAGES;
@@ -296,29 +306,32 @@ __global__ void __launch_bounds__(KD2_THREADS, 1)
     }
     mbar_wait(full + s, (it / STAGES) & 1);
     const double* row = ring + s * STAGE_D + lane * S + c0;
+    if constexpr (kSmemWin) {
+      wsm = row;
+    } else {
 #pragma unroll
-    for (int i = 0; i < WIN / 2; ++i) {
-      const double2 v2 = *reinterpret_cast<const double2*>(row + 2 * i);
-      win[2 * i] = v2.x;
-      win[2 * i + 1] = v2.y;
+      for (int i = 0; i < WIN / 2; ++i) {
+        const double2 v2 = *reinterpret_cast<const double2*>(row + 2 * i);
+        win[2 * i] = v2.x;
+        win[2 * i + 1] = v2.y;
+      }
+      release(it);
     }
   };
-  auto release = [&](int it) {
-    __syncwarp();
-    mbar_arrive_if(empty + it % STAGES, lane == 0);
-  };
-  auto hpass = [&](const double* win, double* hv) {
+  auto hpass = [&](int it, double* hv) {
     if constexpr (KIND == kKindGauss) {
 #pragma unroll
       for (int j = 0; j < KD2_R; ++j) hv[j] = 0.0;
 #pragma unroll
       for (int m = 0; m < KD2_R + 2 * WT; ++m) {
+        const double c = wsm[m];
 #pragma unroll
         for (int j = 0; j < KD2_R; ++j) {
           const int k = m - j;
-          if (k >= 0 && k <= 2 * WT) hv[j] = fma(a.w[k], win[m], hv[j]);
+          if (k >= 0 && k <= 2 * WT) hv[j] = fma(a.w[k], c, hv[j]);
         }
       }
+      release(it);
     } else {
       double s4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -347,23 +360,19 @@ __global__ void __launch_bounds__(KD2_THREADS, 1)
   using T_ = std::true_type;
   using F_ = std::false_type;
 
-  double win[WIN];
   double hv[KD2_R], hn[KD2_R];
-  load_window(0, win);
-  release(0);
-  hpass(win, hv);
+  load_window(0);
+  hpass(0, hv);
   if (N >= 1 && a.mode == kModeGpa) {
-    load_window(1, win);
-    release(1);
+    load_window(1);
     horner(N, hv, F_{}, T_{});
-    hpass(win, hn);
+    hpass(1, hn);
 #pragma unroll
     for (int j = 0; j < KD2_R; ++j) hv[j] = hn[j];
     for (int m = N - 1; m >= 1; --m) {
-      load_window(N - m + 1, win);
-      release(N - m + 1);
+      load_window(N - m + 1);
       horner(m, hv, T_{}, T_{});
-      hpass(win, hn);
+      hpass(N - m + 1, hn);
 #pragma unroll
       for (int j = 0; j < KD2_R; ++j) hv[j] = hn[j];
     }
@@ -457,9 +466,6 @@ int launch_pair64(cudaStream_t st, GpaArgs<double>& a, const KernelEvents& ev) {
 }
 
 }  // namespace fast64
-
-int launch_fast64_gauss(cudaStream_t st, int W, GpaArgs<double>& a, const KernelEvents& ev, bool* done);
-int launch_fast64_box(cudaStream_t st, int W, GpaArgs<double>& a, const KernelEvents& ev, bool* done);
 
 #define FB_CASE64_kKindGauss(w) \
   case w:                       \

@@ -1,0 +1,6 @@
+// fb_tu64_gauss_01.cu — specialised fp64 gauss kernels (fb_fast64.cuh) for half-width groups 01.
+#include "fb_fast64.cuh"
+
+namespace fbgpu {
+FB_FAST64_DISPATCH(launch_fast64_gauss_01, kKindGauss, FB_W_GROUPS_01)
+}  // namespace fbgpu

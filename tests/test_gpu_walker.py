@@ -136,3 +136,21 @@ def test_fp64_fast_kernels_match_oracle_windows(kind, param, N):
         sub = orc.gpa(img[y0:y1, x0:x1].astype(np.float64), kind, W, k.weights_1d, sigma_r, N)
         worst = max(worst, float(np.max(np.abs(out[y:y + h, x:x + w] - sub[y - y0:y - y0 + h, x - x0:x - x0 + w]))))
     assert worst <= 1e-8, worst
+
+
+@pytest.mark.parametrize("kind", ["box", "gaussian"])
+@pytest.mark.parametrize("W", list(range(1, 33)))
+def test_every_fast_half_width(kind, W):
+    """Every half-width 1..32 has specialised kernels in both precisions (fb_tu_*_<group>.cu,
+    fb_tu64_*_<group>.cu): each matches the oracle."""
+    k = (make_spatial_kernel("box", half_width=W) if kind == "box"
+         else make_spatial_kernel("gaussian", sigma_s=(W - 0.5) / 3.0))
+    assert k.half_width == W
+    rng = np.random.default_rng(100 + W)
+    img = np.floor(rng.uniform(0.0, 256.0, (2 * W + 40, 2 * W + 70)))
+    N = 25
+    ref = orc.gpa(img, kind, W, k.weights_1d, 30.0, N)
+    o32 = gpa_filter(img, k, 30.0, N, precision="f32")
+    o64 = gpa_filter(img, k, 30.0, N, precision="f64")
+    assert np.max(np.abs(o32 - ref)) <= F32_TOL
+    assert np.max(np.abs(o64 - ref)) <= 1e-8
