@@ -22,7 +22,7 @@ namespace fbgpu {
 
 constexpr int kMaxW = 160;                  // largest half-width the kernels accept
 constexpr int kMaxTaps = 2 * kMaxW + 1;
-constexpr int kFastMaxW = 32;               // largest half-width of the specialised fp32 kernels
+constexpr int kFastMaxW = 32;               // largest half-width of the specialised kernels
 
 enum : int { kModeGpa = 0, kModePlain = 1 };
 enum : int { kKindBox = 0, kKindGauss = 1 };
