@@ -61,6 +61,31 @@ def test_walker_matches_oracle_and_fp64(W, N, sigma_r, dtype):
     assert _oracle_windows(img, ref64, k, sigma_r, N) <= 1e-8
 
 
+def test_fp64_walker_bands_and_halos_are_exact():
+    """The fp64 walker (fb_fast64.cuh) is partition-independent to fp64 rounding: two bands and a
+    halo-band call reproduce the single call to 1e-10."""
+    torch = pytest.importorskip("torch")
+    img = synth.config_image("c4", height=4096, width=2048)
+    k = make_spatial_kernel("box", half_width=20)
+    N, W = 57, 20
+    dimg = torch.from_numpy(img).cuda()
+    full = gpa_filter(dimg, k, 25.0, N, precision="f64").cpu().numpy()
+    pitch = (2048 + 40 + 31) // 32 * 32
+    _native.set_workspace_limit(2048 * (N + 1) * pitch * 8)
+    try:
+        st = {}
+        banded = gpa_filter(dimg, k, 25.0, N, precision="f64", stats=st).cpu().numpy()
+    finally:
+        _native.set_workspace_limit(8 << 30)
+    assert st["bands"] == 2
+    assert np.max(np.abs(banded - full)) <= 1e-10
+    r0, r1 = 1000, 3100
+    ext = torch.from_numpy(np.ascontiguousarray(img[r0 - W:r1 + W])).cuda()
+    out = torch.empty((r1 - r0, img.shape[1]), dtype=torch.float64, device="cuda")
+    _native.gpa(ext, out, k, 25.0, N, 128.0, 128.0, _native.FB_PREC_F64, 0, halo_top=W, halo_bottom=W)
+    assert np.max(np.abs(out.cpu().numpy() - full[r0:r1])) <= 1e-10
+
+
 def test_walker_band_partitions_agree():
     """Several walker bands (workspace limit) and an explicit halo-band call agree with one band."""
     torch = pytest.importorskip("torch")
