@@ -85,8 +85,10 @@ typedef struct fb_stats {
   double bad_value;             /* its value */
   double device_ms;             /* device time of the whole call (CUDA events), incl. copies */
   double kernel_ms;             /* device time of the filter kernels only */
-  double k1_ms;                 /* of which kernel 1 (channel generation + vertical pass), summed over bands */
-  double k2_ms;                 /* of which kernel 2 (horizontal pass + Horner epilogue), summed over bands */
+  double k1_ms;                 /* of which kernel 1 (channel generation + vertical pass), summed over bands;
+                                   -1 when the call replayed a CUDA graph (small repeated device-resident
+                                   calls: the graph is timed as a whole, kernel_ms = device_ms) */
+  double k2_ms;                 /* of which kernel 2 (horizontal pass + Horner epilogue), same convention */
   int64_t h2d_bytes;
   int64_t d2h_bytes;
   int32_t bands;                /* row bands the workspace limit split the image into */

@@ -98,6 +98,15 @@ __device__ __forceinline__ void store_sample(void* out, int dt, long long idx, d
   else reinterpret_cast<float*>(out)[idx] = (float)v;
 }
 
+// Per-kernel timing events.  Inside a CUDA-graph capture (fb_capi.cu replays small repeated
+// calls) they are skipped: a captured record only orders work, and timestamped external event
+// nodes cost ~13 us per small call; such calls report their kernels' time as one total.
+inline cudaError_t record_timing(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive) return cudaSuccess;
+  return cudaEventRecord(e, s);
+}
+
 template <typename T> __device__ __forceinline__ T gauss_exp(T x);
 template <> __device__ __forceinline__ float gauss_exp<float>(float x) { return expf(-0.5f * x * x); }
 template <> __device__ __forceinline__ double gauss_exp<double>(double x) { return exp(-0.5 * x * x); }

@@ -455,13 +455,13 @@ int launch_pair64(cudaStream_t st, GpaArgs<double>& a, const KernelEvents& ev) {
   dim3 g2((a.cols + KD2_TW - 1) / KD2_TW, (a.band_rows + KD2_TH - 1) / KD2_TH);
   CUtensorMap map;
   if (make_plane_map64(&map, a, W) != 0) return 6;
-  cudaEventRecord(ev.k1_start, st);
+  record_timing(ev.k1_start, st);
   k1<<<g1, b1, s1, st>>>(a);
   if (cudaGetLastError() != cudaSuccess) return 6;
-  cudaEventRecord(ev.k1_end, st);
+  record_timing(ev.k1_end, st);
   k2<<<g2, KD2_THREADS, s2, st>>>(a, map);
   if (cudaGetLastError() != cudaSuccess) return 6;
-  cudaEventRecord(ev.k2_end, st);
+  record_timing(ev.k2_end, st);
   return 0;
 }
 
