@@ -120,7 +120,9 @@ int fb_set_workspace_limit(fb_ctx* ctx, int64_t bytes);
  * Host-resident images of more than 4 MP are processed in 8 row chunks whose
  * copy-in, kernels and copy-out overlap on three streams (pinned host memory
  * makes the copies asynchronous; pageable memory still works, serialised).
- * `out` must be FB_F32 or FB_F64 (the reference returns float64).
+ * `out` may be FB_F64 (the reference's float64 result), FB_F32, or FB_U8: the 8-bit raster that
+ * save_pgm / save_image write (image.py:96-99, :122-127), quantised as floor(clip(v, 0, 255) + 0.5)
+ * in kernel 2's epilogue, so a PGM/PNG pipeline moves 1 byte per pixel each way.
  * The caller validates sigma_r and the order (engine.py:40-49) and the box
  * window (conv.py:19-27); they are re-checked here and reported as FB_ERR_PARAM.
  */
@@ -162,6 +164,32 @@ int fb_validate(fb_ctx* ctx, const fb_image* in, double lo, double hi, fb_stats*
  */
 int fb_bilateral_exact(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_spatial* spatial,
                        double sigma_r, fb_stats* stats);
+
+/*
+ * fb_convolve_direct — replaces convolve_direct (conv.py:83-96): the literal O(W^2) double sum
+ * out(i) = sum_j w(j) f(i - j) with the (2W+1)^2 table `weights_2d` (SpatialKernel.weights,
+ * row-major, origin at [W][W]), replicate boundary, accumulated in the reference's order in fp64
+ * without contraction.  `out` must be FB_F64.  FB_ERR_WINDOW if W >= min(dims > 1) (conv.py:19-27).
+ */
+int fb_convolve_direct(fb_ctx* ctx, const fb_image* in, fb_image* out, int32_t half_width, const double* weights_2d,
+                       fb_stats* stats);
+
+/*
+ * fb_error_stats — replaces the reductions of linf_error / mse_db (analysis.py:33-46):
+ * *linf = max |a - b|, *sum_sq = sum (a - b)^2 over all pixels, in fp64.  Both images are checked
+ * for finiteness first (as_image, image.py:35-42): FB_ERR_NONFINITE_INPUT with stats->bad_image
+ * (0 = a, 1 = b) and bad_index.  Shapes must match (FB_ERR_PARAM "image dimensions differ").
+ */
+int fb_error_stats(fb_ctx* ctx, const fb_image* a, const fb_image* b, double* linf, double* sum_sq,
+                   fb_stats* stats);
+
+/*
+ * fb_kernel_error_sup — replaces kernel_error_sup (analysis.py:70-103): the worst-case kernel error
+ * of the order-`order` approximant over the integer grid t, tau in {-floor(T) .. floor(T)}, through
+ * the tail series exp(-(t^2 + tau^2)/2 sigma_r^2) sum_{n >= N} (t tau / sigma_r^2)^n / n!, one
+ * device thread per grid point.  FB_ERR_PARAM for order < 1 or non-positive sigma_r / T.
+ */
+int fb_kernel_error_sup(fb_ctx* ctx, int32_t order, double sigma_r, double half_range, double* sup);
 
 /*
  * Peer output buffers for the row-band partitioning (north star item 5: "no collective beyond a

@@ -3,30 +3,36 @@
 The public names mirror `/root/reference/pkg/src/fastbilateral/__init__.py:35-48`
 for the hot path (§8 of SURVEY.md): the filter (`gpa_filter`,
 `gpa_filter_auto`), the spatial filters it applies (`apply_spatial`,
-`box_filter`, `gaussian_filter`), kernels, range handling, order selection and
-the error types.  Filtering runs in hand-written sm_100a CUDA kernels
+`box_filter`, `gaussian_filter`, `convolve_direct`), kernels, range handling,
+order selection and the error types; and the tools around it (§8(f)): the
+exact filter, error metrology (`analysis`), PGM/PNG I/O and the CLI (`cli`).  Filtering runs in hand-written sm_100a CUDA kernels
 (`csrc/`, loaded from the in-tree `libfbgpu.so` through `_native`); there is
 no CPU fallback.
 """
 
-from .conv import apply_spatial, box_filter, gaussian_filter
+from .analysis import (ErrorReport, accuracy_bound, error_report, kernel_error_sup, linf_error, mse_db,
+                       psi_eval)
+from .conv import apply_spatial, box_filter, convolve_direct, gaussian_filter
 from .engine import gpa_filter, gpa_filter_auto, gpa_filter_batch
 from .errors import (BoundInapplicableError, NativeError, NumericRangeError, ParameterError,
                      RangeViolationError)
-from .image import RANGE_8BIT, RangeSpec, as_image, center, uncenter, validate_range
-from .kernels import SpatialKernel, make_spatial_kernel
+from .image import (RANGE_8BIT, RangeSpec, as_image, center, load_image, load_pgm, quantize, read_raster,
+                    save_image, save_pgm, uncenter, validate_range, write_raster)
+from .kernels import SpatialKernel, gauss_poly, make_spatial_kernel, range_kernel
 from .reference import bilateral_exact
-from .order import (OrderEstimate, chernoff_order_exhaustive, epsilon_from_delta, estimate_order,
-                    lambert_w0_series, log_chernoff)
+from .order import (OrderEstimate, chebyshev_order, chernoff_order_exhaustive, epsilon_from_delta,
+                    estimate_order, lambert_w0_series, log_chernoff, order_approx, poisson_tail, yang_order)
 
 __version__ = "1.0.0"
 
 __all__ = [
-    "OrderEstimate", "RangeSpec", "SpatialKernel", "RANGE_8BIT", "__version__",
-    "apply_spatial", "as_image", "bilateral_exact", "box_filter", "center", "chernoff_order_exhaustive",
-    "epsilon_from_delta", "estimate_order", "gaussian_filter", "gpa_filter", "gpa_filter_auto",
-    "gpa_filter_batch",
-    "lambert_w0_series", "log_chernoff", "make_spatial_kernel", "uncenter", "validate_range",
+    "ErrorReport", "OrderEstimate", "RangeSpec", "SpatialKernel", "RANGE_8BIT", "__version__",
+    "accuracy_bound", "apply_spatial", "as_image", "bilateral_exact", "box_filter", "center",
+    "chebyshev_order", "chernoff_order_exhaustive", "convolve_direct", "epsilon_from_delta", "error_report",
+    "estimate_order", "gauss_poly", "gaussian_filter", "gpa_filter", "gpa_filter_auto", "gpa_filter_batch",
+    "kernel_error_sup", "lambert_w0_series", "linf_error", "load_image", "load_pgm", "log_chernoff",
+    "make_spatial_kernel", "mse_db", "order_approx", "poisson_tail", "psi_eval", "quantize", "range_kernel",
+    "read_raster", "save_image", "save_pgm", "uncenter", "validate_range", "write_raster", "yang_order",
     "BoundInapplicableError", "NativeError", "NumericRangeError", "ParameterError",
     "RangeViolationError",
 ]

@@ -29,7 +29,8 @@ FB_PREC_F32, FB_PREC_F64 = 1, 2
 EXPORTED_SYMBOLS = (
     "fb_create", "fb_destroy", "fb_set_stream", "fb_set_workspace_limit", "fb_gpa_filter",
     "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate", "fb_bilateral_exact", "fb_last_error",
-    "fb_version", "fb_launch_count", "fb_ipc_export", "fb_ipc_open", "fb_ipc_close",
+    "fb_version", "fb_launch_count", "fb_ipc_export", "fb_ipc_open", "fb_ipc_close", "fb_convolve_direct",
+    "fb_error_stats", "fb_kernel_error_sup",
 )
 
 
@@ -72,6 +73,9 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         if not os.path.exists(path):
             raise NativeError(f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
         lib = ctypes.CDLL(path)
+        missing = [n for n in EXPORTED_SYMBOLS if not hasattr(lib, n)]
+        if missing:
+            raise NativeError(f"{path} lacks {', '.join(missing)}: stale build, rerun __graft_entry__.build()")
         P = ctypes.POINTER
         vp = ctypes.c_void_p
         lib.fb_create.argtypes = [ctypes.c_int, P(vp)]
@@ -90,11 +94,18 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         lib.fb_spatial_filter.argtypes = [vp, P(FbImage), P(FbImage), P(FbSpatial), ctypes.c_int32, P(FbStats)]
         lib.fb_validate.argtypes = [vp, P(FbImage), ctypes.c_double, ctypes.c_double, P(FbStats)]
         lib.fb_bilateral_exact.argtypes = [vp, P(FbImage), P(FbImage), P(FbSpatial), ctypes.c_double, P(FbStats)]
+        lib.fb_convolve_direct.argtypes = [vp, P(FbImage), P(FbImage), ctypes.c_int32, P(ctypes.c_double),
+                                           P(FbStats)]
+        lib.fb_error_stats.argtypes = [vp, P(FbImage), P(FbImage), P(ctypes.c_double), P(ctypes.c_double),
+                                       P(FbStats)]
+        lib.fb_kernel_error_sup.argtypes = [vp, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
+                                            P(ctypes.c_double)]
         lib.fb_last_error.restype = ctypes.c_char_p
         lib.fb_version.restype = ctypes.c_int
         lib.fb_launch_count.restype = ctypes.c_int64
         for name in ("fb_create", "fb_destroy", "fb_set_stream", "fb_set_workspace_limit", "fb_gpa_filter",
-                     "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate", "fb_bilateral_exact"):
+                     "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate", "fb_bilateral_exact",
+                     "fb_convolve_direct", "fb_error_stats", "fb_kernel_error_sup"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
         return lib
@@ -143,6 +154,8 @@ def image_desc(arr) -> FbImage:
             raise ValueError("tensor rows must be contiguous")
         return FbImage(arr.data_ptr(), _TORCH_DT[str(arr.dtype)], 1, arr.shape[0], arr.shape[1], rs)
     isz = arr.itemsize
+    if arr.shape[0] == 1:  # a single row: its row stride is irrelevant (numpy may report 0)
+        return FbImage(arr.ctypes.data, _NP_DT[arr.dtype], 0, 1, arr.shape[1], arr.shape[1])
     if arr.strides[1] != isz or arr.strides[0] % isz or arr.strides[0] < arr.shape[1] * isz:
         raise ValueError("array rows must be contiguous")
     return FbImage(arr.ctypes.data, _NP_DT[arr.dtype], 0, arr.shape[0], arr.shape[1], arr.strides[0] // isz)
@@ -273,3 +286,40 @@ def validate(src, lo: float, hi: float, device: int = 0) -> None:
     st = FbStats()
     rc = lib.fb_validate(ctx, ctypes.byref(image_desc(src)), float(lo), float(hi), ctypes.byref(st))
     _check(lib, rc, src, st, lo, hi)
+
+
+def convolve_direct(src, out, weights_2d: np.ndarray, half_width: int, device: int = 0) -> dict:
+    """fb_convolve_direct: the literal 2-D convolution with the (2W+1)^2 table (conv.py:83-96)."""
+    lib = load_library()
+    ctx = context(device)
+    lib.fb_set_stream(ctx, _stream_for(src, device))
+    w2 = np.ascontiguousarray(weights_2d, dtype=np.float64)
+    st = FbStats()
+    rc = lib.fb_convolve_direct(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)), int(half_width),
+                                w2.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(st))
+    _check(lib, rc, src, st)
+    return st.as_dict()
+
+
+def error_stats(a, b, device: int = 0) -> tuple[float, float]:
+    """fb_error_stats: (max |a - b|, sum (a - b)^2) in fp64 on the device (analysis.py:33-46)."""
+    lib = load_library()
+    ctx = context(device)
+    lib.fb_set_stream(ctx, _stream_for(a, device))
+    linf, ss = ctypes.c_double(0.0), ctypes.c_double(0.0)
+    st = FbStats()
+    rc = lib.fb_error_stats(ctx, ctypes.byref(image_desc(a)), ctypes.byref(image_desc(b)), ctypes.byref(linf),
+                            ctypes.byref(ss), ctypes.byref(st))
+    _check(lib, rc, a, st)
+    return float(linf.value), float(ss.value)
+
+
+def kernel_error_sup(order: int, sigma_r: float, half_range: float, device: int = 0) -> float:
+    """fb_kernel_error_sup: grid supremum of the kernel error (analysis.py:70-103)."""
+    lib = load_library()
+    ctx = context(device)
+    lib.fb_set_stream(ctx, ctypes.c_void_p(None))
+    sup = ctypes.c_double(0.0)
+    rc = lib.fb_kernel_error_sup(ctx, int(order), float(sigma_r), float(half_range), ctypes.byref(sup))
+    _check(lib, rc, None, None)
+    return float(sup.value)

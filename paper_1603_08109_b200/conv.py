@@ -6,7 +6,9 @@ each channel, exposed for one image.  They run the same two CUDA kernels in
 "plain" mode (channel = the image itself, no Horner epilogue).  Default
 precision is fp64 so results agree with the reference's fp64 numpy filters to
 ~1e-12; `precision="f32"` is available for large images.
-The literal O(W^2) `convolve_direct` oracle stays on the host side (`oracle/`).
+`convolve_direct` (`conv.py:83-96`), the literal O(W^2) double sum with the 2-D weight table that
+the reference uses as its convolution oracle, runs as its own device kernel
+(`fb_convolve_direct`), accumulated in the reference's order without FMA contraction.
 """
 
 from __future__ import annotations
@@ -62,3 +64,18 @@ def gaussian_filter(img, sigma_s: float, *, precision: str = "f64", device: int 
 def apply_spatial(img, kernel: SpatialKernel, *, precision: str = "f64", device: int | None = None):
     """Filter with a constructed kernel (conv.py:75-80): box checks its window, Gaussian does not."""
     return _run(img, kernel, precision, device, kernel.kind == "box")
+
+
+def convolve_direct(img, kernel: SpatialKernel, *, device: int | None = None):
+    """Literal double-sum convolution out(i) = sum_j w(j) img(i - j), 2-D table, replicate boundary
+    (conv.py:83-96); fp64, float64 result.  The window check applies to every kernel kind."""
+    a, is_dev = _coerce(img)
+    shape = _shape_check(a)
+    dev = _native.device_of(a, device)
+    err = _gauss_window_error(kernel, shape)
+    if err is not None:
+        _native.validate(a, -np.inf, np.inf, dev)
+        raise err
+    out = _alloc_out(a, is_dev, shape, np.float64)
+    _native.convolve_direct(a, out, kernel.weights, kernel.half_width, dev)
+    return out

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "../../include/fbgpu.h"
+#include "fb_analysis.cuh"
 #include "fb_common.cuh"
 #include "fb_generic.cuh"
 #include "fb_fast.cuh"
@@ -101,6 +102,10 @@ struct fb_ctx {
   int tab_n = -1;                            // order N the table currently holds
   long long ws_limit = 0;
   int sm_count = 148;
+  // small device scratch + pinned readback for the reductions of fb_error_stats / fb_kernel_error_sup
+  double* scratch = nullptr;
+  double* scratch_host = nullptr;
+  size_t scratch_cap = 0;                    // doubles
   cudaEvent_t ev_start = nullptr, ev_kstart = nullptr, ev_kend = nullptr, ev_end = nullptr;
   // Per-band kernel boundaries: [k1 start, k1 end = k2 start, k2 end] x bands.
   std::vector<cudaEvent_t> kev;
@@ -706,29 +711,34 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
 // bilateral_exact (reference.py:17-45), used to report the GPA approximation error at full size.
 // CTA = 16x16 outputs; the (16+2W)^2 input tile (clamped rows/columns) is staged in shared memory.
 constexpr int BF_T = 16;
+constexpr int BF_MAX_TILED_W = 77;  // (16 + 2W)^2 doubles fit the 227 KB of shared memory
 
+template <bool TILED>
 __global__ void __launch_bounds__(BF_T * BF_T) k_bilateral_exact(const void* f, long long f_ld, int f_dtype,
                                                                  int rows, int cols, int W, const double* w1d,
                                                                  double inv_two_sr2, double* out, long long out_ld) {
   extern __shared__ double bf_tile[];
   const int S = BF_T + 2 * W;
   const int y0 = blockIdx.y * BF_T, x0 = blockIdx.x * BF_T;
-  for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
-    const int ty = i / S, tx = i - ty * S;
-    const int gy = min(max(y0 + ty - W, 0), rows - 1), gx = min(max(x0 + tx - W, 0), cols - 1);
-    bf_tile[i] = load_sample(f, f_dtype, (long long)gy * f_ld + gx);
+  if (TILED) {
+    for (int i = threadIdx.x; i < S * S; i += blockDim.x) {
+      const int ty = i / S, tx = i - ty * S;
+      const int gy = min(max(y0 + ty - W, 0), rows - 1), gx = min(max(x0 + tx - W, 0), cols - 1);
+      bf_tile[i] = load_sample(f, f_dtype, (long long)gy * f_ld + gx);
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const int ty = threadIdx.x / BF_T, tx = threadIdx.x % BF_T;
   const int y = y0 + ty, x = x0 + tx;
   if (y >= rows || x >= cols) return;
-  const double fi = bf_tile[(ty + W) * S + tx + W];
+  const double fi = TILED ? bf_tile[(ty + W) * S + tx + W] : load_sample(f, f_dtype, (long long)y * f_ld + x);
   double num = 0.0, den = 0.0;
   for (int dy = 0; dy <= 2 * W; ++dy) {
     const double wy = w1d[dy];
     const double* rowp = bf_tile + (ty + dy) * S + tx;
+    const long long grow_ = (long long)min(max(y + dy - W, 0), rows - 1) * f_ld;
     for (int dx = 0; dx <= 2 * W; ++dx) {
-      const double nb = rowp[dx];
+      const double nb = TILED ? rowp[dx] : load_sample(f, f_dtype, grow_ + min(max(x + dx - W, 0), cols - 1));
       const double d = nb - fi;
       const double wgt = wy * w1d[dx] * exp(-d * d * inv_two_sr2);
       num = fma(wgt, nb, num);
@@ -826,7 +836,8 @@ int fb_destroy(fb_ctx* c) {
   for (void* p : {c->ws, c->ws2, c->in_stage[0], c->in_stage[1], c->out_stage[0], c->out_stage[1], (void*)c->flags,
                   (void*)c->tab, (void*)c->tabd})
     if (p) cudaFree(p);
-  for (void* p : {(void*)c->flags_host, (void*)c->tab_host, (void*)c->tabd_host})
+  if (c->scratch) cudaFree(c->scratch);
+  for (void* p : {(void*)c->flags_host, (void*)c->tab_host, (void*)c->tabd_host, (void*)c->scratch_host})
     if (p) cudaFreeHost(p);
   for (cudaEvent_t e : {c->ev_start, c->ev_kstart, c->ev_kend, c->ev_end})
     if (e) cudaEventDestroy(e);
@@ -885,7 +896,7 @@ static int gpa_common(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int coun
   for (int i = 0; i < count; ++i) {
     rc = check_image(ins + i, "input", true);
     if (rc) return rc;
-    rc = check_image(outs + i, "output", false);
+    rc = check_image(outs + i, "output", true);  // u8: quantised raster (save_pgm, image.py:96-99)
     if (rc) return rc;
     if (halo_top < 0 || halo_bottom < 0 || halo_top + halo_bottom >= ins[i].rows)
       return fail(FB_ERR_PARAM, "bad halo rows");
@@ -1005,13 +1016,15 @@ int fb_bilateral_exact(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_
     dout = ctx->out_stage[0];
     old = out->cols;
   }
-  const size_t smem = (size_t)(BF_T + 2 * W) * (BF_T + 2 * W) * sizeof(double);
-  FB_CUDA(cudaFuncSetAttribute(k_bilateral_exact, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const bool tiled = W <= BF_MAX_TILED_W;
+  const size_t smem = tiled ? (size_t)(BF_T + 2 * W) * (BF_T + 2 * W) * sizeof(double) : 0;
+  if (tiled)
+    FB_CUDA(cudaFuncSetAttribute(k_bilateral_exact<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)((in->cols + BF_T - 1) / BF_T), (unsigned)((in->rows + BF_T - 1) / BF_T));
   FB_CUDA(record_timing(ctx->ev_kstart, ctx->stream));
-  k_bilateral_exact<<<grid, BF_T * BF_T, smem, ctx->stream>>>(din, dld, in->dtype, (int)in->rows, (int)in->cols, W,
-                                                                dw, 1.0 / (2.0 * sigma_r * sigma_r),
-                                                                static_cast<double*>(dout), old);
+  (tiled ? k_bilateral_exact<true> : k_bilateral_exact<false>)<<<grid, BF_T * BF_T, smem, ctx->stream>>>(
+      din, dld, in->dtype, (int)in->rows, (int)in->cols, W, dw, 1.0 / (2.0 * sigma_r * sigma_r),
+      static_cast<double*>(dout), old);
   FB_CUDA(cudaGetLastError());
   g_launches += 1;
   FB_CUDA(record_timing(ctx->ev_kend, ctx->stream));
@@ -1030,6 +1043,196 @@ int fb_bilateral_exact(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_
   local.precision = FB_PREC_F64;
   if (stats) *stats = local;
   return FB_OK;
+}
+
+// ---------------------------------------------------------------------------- metrology / oracle
+static int ensure_scratch(fb_ctx* c, size_t doubles) {
+  if (doubles <= c->scratch_cap) return FB_OK;
+  if (c->scratch) cudaFree(c->scratch);
+  if (c->scratch_host) cudaFreeHost(c->scratch_host);
+  c->scratch = nullptr;
+  c->scratch_host = nullptr;
+  c->scratch_cap = 0;
+  FB_CUDA(cudaMalloc(&c->scratch, doubles * sizeof(double)));
+  FB_CUDA(cudaMallocHost(&c->scratch_host, doubles * sizeof(double)));
+  c->scratch_cap = doubles;
+  return FB_OK;
+}
+
+// Device copy of a host image into staging slot `slot` (or the image itself when on the device).
+static int stage_input(fb_ctx* c, const fb_image* im, int slot, const void** d, long long* ld) {
+  if (im->on_device) {
+    *d = im->data;
+    *ld = im->ld;
+    return FB_OK;
+  }
+  const size_t es = dtype_size(im->dtype);
+  int rc = grow(&c->in_stage[slot], &c->in_stage_bytes[slot], (size_t)im->rows * im->cols * es);
+  if (rc) return rc;
+  FB_CUDA(cudaMemcpy2DAsync(c->in_stage[slot], im->cols * es, im->data, im->ld * es, im->cols * es, im->rows,
+                            cudaMemcpyHostToDevice, c->stream));
+  *d = c->in_stage[slot];
+  *ld = im->cols;
+  return FB_OK;
+}
+
+int fb_kernel_error_sup(fb_ctx* ctx, int32_t order, double sigma_r, double half_range, double* sup) {
+  if (!ctx || !sup) return fail(FB_ERR_PARAM, "null argument");
+  if (order < 1) return fail(FB_ERR_PARAM, "N must be >= 1, got " + std::to_string(order));
+  if (!(sigma_r > 0 && half_range > 0)) return fail(FB_ERR_PARAM, "sigma_r and T must be positive");
+  if (!(half_range < 1e6)) return fail(FB_ERR_PARAM, "T too large for the grid search");
+  FB_CUDA(cudaSetDevice(ctx->device));
+  int rc = ensure_scratch(ctx, 64);
+  if (rc) return rc;
+  unsigned long long* bits = reinterpret_cast<unsigned long long*>(ctx->scratch);
+  FB_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned long long), ctx->stream));
+  if (launch_kernel_error_sup(ctx->stream, ctx->sm_count, (int)std::floor(half_range), order, sigma_r, bits))
+    return fail(FB_ERR_CUDA, "kernel_error_sup launch failed");
+  g_launches += 1;
+  FB_CUDA(cudaMemcpyAsync(ctx->scratch_host, bits, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  FB_CUDA(cudaStreamSynchronize(ctx->stream));
+  *sup = ctx->scratch_host[0];
+  return FB_OK;
+}
+
+int fb_error_stats(fb_ctx* ctx, const fb_image* a, const fb_image* b, double* linf, double* sum_sq,
+                   fb_stats* stats) {
+  if (!ctx || !linf || !sum_sq) return fail(FB_ERR_PARAM, "null argument");
+  int rc = check_image(a, "a", true);
+  if (rc) return rc;
+  rc = check_image(b, "b", true);
+  if (rc) return rc;
+  if (a->rows != b->rows || a->cols != b->cols)
+    return fail(FB_ERR_PARAM, "image dimensions differ: (" + std::to_string(a->rows) + ", " +
+                                  std::to_string(a->cols) + ") vs (" + std::to_string(b->rows) + ", " +
+                                  std::to_string(b->cols) + ")");
+  FB_CUDA(cudaSetDevice(ctx->device));
+  const int nb = error_stats_blocks(ctx->sm_count);
+  rc = ensure_scratch(ctx, 2 * (size_t)nb + 4);
+  if (rc) return rc;
+  rc = ensure_flags(ctx, 2);
+  if (rc) return rc;
+  fb_stats local;
+  memset(&local, 0, sizeof(local));
+  local.bad_image = -1;
+  FB_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
+  FB_CUDA(cudaMemcpyAsync(ctx->flags, ctx->flags_host, 8 * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  const void *da = nullptr, *db = nullptr;
+  long long lda = 0, ldb = 0;
+  if ((rc = stage_input(ctx, a, 0, &da, &lda)) || (rc = stage_input(ctx, b, 1, &db, &ldb))) return rc;
+  local.h2d_bytes = (a->on_device ? 0 : a->rows * a->cols * (long long)dtype_size(a->dtype)) +
+                    (b->on_device ? 0 : b->rows * b->cols * (long long)dtype_size(b->dtype));
+  FB_CUDA(record_timing(ctx->ev_kstart, ctx->stream));
+  if (launch_error_stats(ctx->stream, ctx->sm_count, da, lda, a->dtype, db, ldb, b->dtype, (int)a->rows,
+                         (int)a->cols, ctx->scratch, ctx->flags + kFlagFirstNonfinite,
+                         ctx->flags + 4 + kFlagFirstNonfinite))
+    return fail(FB_ERR_CUDA, "error_stats launch failed");
+  g_launches += 1;
+  FB_CUDA(record_timing(ctx->ev_kend, ctx->stream));
+  unsigned long long* fl = ctx->flags_host + 4 * ctx->flags_cap;
+  FB_CUDA(cudaMemcpyAsync(ctx->scratch_host, ctx->scratch, 2 * (size_t)nb * sizeof(double), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  FB_CUDA(cudaMemcpyAsync(fl, ctx->flags, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  FB_CUDA(cudaEventRecord(ctx->ev_end, ctx->stream));
+  FB_CUDA(cudaEventSynchronize(ctx->ev_end));
+  double mx = 0.0, ss = 0.0;
+  for (int i = 0; i < nb; ++i) {
+    mx = std::max(mx, ctx->scratch_host[2 * i]);
+    ss += ctx->scratch_host[2 * i + 1];
+  }
+  *linf = mx;
+  *sum_sq = ss;
+  float ms = 0.f, kms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_end);
+  cudaEventElapsedTime(&kms, ctx->ev_kstart, ctx->ev_kend);
+  local.device_ms = ms;
+  local.kernel_ms = kms;
+  local.launches = 1;
+  local.precision = FB_PREC_F64;
+  int status = FB_OK;
+  for (int i = 0; i < 2 && status == FB_OK; ++i) {
+    const unsigned long long idx = fl[4 * i + kFlagFirstNonfinite];
+    if (idx == ~0ull) continue;
+    local.bad_image = i;
+    local.bad_index = (long long)idx;
+    status = fail(FB_ERR_NONFINITE_INPUT, "image contains non-finite samples");
+  }
+  if (stats) *stats = local;
+  return status;
+}
+
+int fb_convolve_direct(fb_ctx* ctx, const fb_image* in, fb_image* out, int32_t half_width, const double* weights_2d,
+                       fb_stats* stats) {
+  if (!ctx || !weights_2d) return fail(FB_ERR_PARAM, "null argument");
+  int rc = check_image(in, "input", true);
+  if (rc) return rc;
+  rc = check_image(out, "output", false);
+  if (rc) return rc;
+  if (out->dtype != FB_F64 || out->rows != in->rows || out->cols != in->cols)
+    return fail(FB_ERR_PARAM, "output must be float64 of the input's shape");
+  if (half_width < 1 || half_width > kMaxW)
+    return fail(FB_ERR_PARAM, "half_width must lie in [1, " + std::to_string(kMaxW) + "]");
+  fb_spatial sp{FB_BOX, half_width, nullptr};  // _check_window applies to every kind here (conv.py:86)
+  rc = check_window(&sp, in->rows, in->cols);
+  if (rc) return rc;
+  FB_CUDA(cudaSetDevice(ctx->device));
+  const int n = 2 * half_width + 1;
+  rc = ensure_flags(ctx, 1);
+  if (rc) return rc;
+  fb_stats local;
+  memset(&local, 0, sizeof(local));
+  local.bad_image = -1;
+  FB_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
+  // as_image's finiteness check first (conv.py:85), on the staged input
+  FB_CUDA(cudaMemcpyAsync(ctx->flags, ctx->flags_host, 4 * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                          ctx->stream));
+  const void* din = nullptr;
+  long long dld = 0;
+  if ((rc = stage_input(ctx, in, 0, &din, &dld))) return rc;
+  if (launch_validate(ctx->stream, din, dld, in->dtype, (int)in->rows, (int)in->cols, -INFINITY, INFINITY,
+                      ctx->flags, ctx->sm_count))
+    return fail(FB_ERR_CUDA, "validation kernel launch failed");
+  double* dw = nullptr;
+  FB_CUDA(cudaMallocAsync(&dw, (size_t)n * n * sizeof(double), ctx->stream));
+  FB_CUDA(cudaMemcpyAsync(dw, weights_2d, (size_t)n * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  void* dout = out->data;
+  long long old = out->ld;
+  if (!out->on_device) {
+    rc = grow(&ctx->out_stage[0], &ctx->out_stage_bytes[0], (size_t)out->rows * out->cols * 8);
+    if (rc) return rc;
+    dout = ctx->out_stage[0];
+    old = out->cols;
+  }
+  FB_CUDA(record_timing(ctx->ev_kstart, ctx->stream));
+  if (launch_convolve_direct(ctx->stream, din, dld, in->dtype, (int)in->rows, (int)in->cols, half_width, dw,
+                             static_cast<double*>(dout), old))
+    return fail(FB_ERR_CUDA, "convolve_direct launch failed");
+  g_launches += 2;
+  FB_CUDA(record_timing(ctx->ev_kend, ctx->stream));
+  if (!out->on_device)
+    FB_CUDA(cudaMemcpy2DAsync(out->data, out->ld * 8, dout, old * 8, out->cols * 8, out->rows,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+  unsigned long long* fl = ctx->flags_host + 4 * ctx->flags_cap;
+  FB_CUDA(cudaMemcpyAsync(fl, ctx->flags, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream));
+  FB_CUDA(cudaFreeAsync(dw, ctx->stream));
+  FB_CUDA(cudaEventRecord(ctx->ev_end, ctx->stream));
+  FB_CUDA(cudaEventSynchronize(ctx->ev_end));
+  float ms = 0.f, kms = 0.f;
+  cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_end);
+  cudaEventElapsedTime(&kms, ctx->ev_kstart, ctx->ev_kend);
+  local.device_ms = ms;
+  local.kernel_ms = kms;
+  local.launches = 2;
+  local.precision = FB_PREC_F64;
+  int status = FB_OK;
+  if (fl[kFlagFirstNonfinite] != ~0ull) {
+    local.bad_index = (long long)fl[kFlagFirstNonfinite];
+    local.bad_image = 0;
+    status = fail(FB_ERR_NONFINITE_INPUT, "image contains non-finite samples");
+  }
+  if (stats) *stats = local;
+  return status;
 }
 
 }  // extern "C"

@@ -11,7 +11,7 @@
 //                  of a row puts all N+1 stores of one output row within a few MB of each
 //                  other (immediate-offset stores); kernel 2 fetches per-channel tiles with
 //                  a 3-D TMA map {pitch, N+1, rows}.
-//   output       : row-major f32/f64, leading dim out_ld.
+//   output       : row-major u8/f32/f64, leading dim out_ld.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -59,7 +59,7 @@ struct GpaArgs {
   // output
   void* out;
   long long out_ld;
-  int out_dtype;      // 1 f32, 2 f64
+  int out_dtype;      // 0 u8 (quantised as save_pgm does), 1 f32, 2 f64
   unsigned long long* flags;
   // fp32 channel constants, 4 per channel m: r_m = fl32(1/sqrt(m)) (0 for m = 0), sqrt(m),
   // and the matched Horner constants h_m = 1/(m r_m), s_m = 1/r_m rounded to fp32
@@ -93,9 +93,18 @@ __device__ __forceinline__ double load_sample(const void* f, int dt, long long i
   return (double)__ldg(reinterpret_cast<const unsigned char*>(f) + idx);
 }
 
+// 8-bit output sample: clamp to [0, 255], round half up — save_pgm / save_image's quantisation
+// floor(clip(x, 0, 255) + 0.5) (image.py:96-99, :122-127).  Non-finite values (which make the
+// call fail with FB_ERR_NUMERIC anyway) store 0.
+__device__ __forceinline__ unsigned quantize_u8(double v) {
+  if (!isfinite(v)) return 0u;
+  return (unsigned)floor(fmin(fmax(v, 0.0), 255.0) + 0.5);
+}
+
 __device__ __forceinline__ void store_sample(void* out, int dt, long long idx, double v) {
   if (dt == 2) reinterpret_cast<double*>(out)[idx] = v;
-  else reinterpret_cast<float*>(out)[idx] = (float)v;
+  else if (dt == 1) reinterpret_cast<float*>(out)[idx] = (float)v;
+  else reinterpret_cast<unsigned char*>(out)[idx] = (unsigned char)quantize_u8(v);
 }
 
 // Per-kernel timing events.  Inside a CUDA-graph capture (fb_capi.cu replays small repeated

@@ -73,3 +73,27 @@ def make_spatial_kernel(kind: str, *, sigma_s: float | None = None,
     if kind == "gaussian":
         return _gaussian(sigma_s)
     raise ParameterError(f"unknown spatial kernel kind {kind!r}")
+
+
+def range_kernel(t, sigma_r: float):
+    """Gaussian range kernel exp(-t^2 / (2 sigma_r^2)), elementwise (kernels.py:33-37)."""
+    if not sigma_r > 0:
+        raise ParameterError(f"sigma_r must be positive, got {sigma_r}")
+    t = np.asarray(t, dtype=np.float64)
+    return np.exp(-np.square(t) / (2.0 * sigma_r**2))
+
+
+def gauss_poly(t: float, tau: float, order: int, sigma_r: float) -> float:
+    """Order-N approximant of the translated range kernel (kernels.py:40-58):
+    exp(-(t^2 + tau^2) / 2 sigma_r^2) times the first `order` Taylor terms of exp(t tau / sigma_r^2),
+    summed by the term recursion (no factorials)."""
+    if not sigma_r > 0:
+        raise ParameterError(f"sigma_r must be positive, got {sigma_r}")
+    if order < 1:
+        raise ParameterError(f"order must be >= 1, got {order}")
+    x = (t * tau) / sigma_r**2
+    term = acc = 1.0
+    for n in range(1, order):
+        term *= x / n
+        acc += term
+    return math.exp(-(t * t + tau * tau) / (2.0 * sigma_r**2)) * acc

@@ -20,12 +20,17 @@ def bilateral_exact(img, spatial: SpatialKernel, sigma_r: float, *, device: int 
     a, is_dev = _coerce(img)
     shape = _shape_check(a)
     dev = _native.device_of(a, device)
-    if not sigma_r > 0:
-        raise ParameterError(f"sigma_r must be positive, got {sigma_r}")
     W = spatial.half_width
-    if W >= min(shape):
-        raise ParameterError(f"window half-width {W} too large for {shape[0]}x{shape[1]} image")
-    _native.validate(a, -np.inf, np.inf, dev)  # as_image: finite samples only
+    err = None
+    if not sigma_r > 0:
+        err = ParameterError(f"sigma_r must be positive, got {sigma_r}")
+    elif W >= min(shape):
+        err = ParameterError(f"window half-width {W} too large for {shape[0]}x{shape[1]} image")
+    # as_image (finite samples only) runs first in the reference (reference.py:24), so a bad image
+    # is reported before a bad parameter
+    _native.validate(a, -np.inf, np.inf, dev)
+    if err is not None:
+        raise err
     out = _alloc_out(a, is_dev, shape, np.float64)
     _native.bilateral_exact(a, out, spatial, float(sigma_r), dev)
     return out

@@ -40,3 +40,15 @@ def random_image(rng):
         r = rng if seed is None else np.random.default_rng(seed)
         return np.floor(r.uniform(0.0, 256.0, (h, w)))
     return make
+
+
+@pytest.fixture(scope="session")
+def tools_golden():
+    """Reference outputs for I/O, metrology, convolve_direct and the CLI (make_golden_tools.py)."""
+    return np.load(os.path.join(GOLDEN_DIR, "reference_tools.npz"))
+
+
+@pytest.fixture(scope="session")
+def tools_scalars():
+    with open(os.path.join(GOLDEN_DIR, "reference_tools.json")) as fh:
+        return json.load(fh)

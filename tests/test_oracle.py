@@ -75,3 +75,20 @@ def test_oracle_q_floor_case(golden):
     # order 1, sigma_r 10, 255 impulse: the reference passes some pixels through
     out = orc.gpa(golden["qdegenerate5_in"], "box", 1, np.full(3, 1 / 3), 10.0, 1)
     assert np.all(np.isfinite(out))
+
+
+# ----------------------------------------------------------------------------- tools (§8(f) rows 3-4)
+def test_oracle_tools_pinned(tools_golden, tools_scalars):
+    from paper_1603_08109_b200 import make_spatial_kernel
+    for name, c in tools_scalars["convolve_direct"].items():
+        k = make_spatial_kernel(c["kind"], **({"half_width": c["param"]} if c["kind"] == "box"
+                                              else {"sigma_s": c["param"]}))
+        out = orc.convolve_2d(tools_golden[f"conv_{name}_in"], k.weights, k.half_width)
+        assert np.array_equal(out, tools_golden[f"conv_{name}_out"]), name
+    for n, s, t, v in tools_scalars["kernel_error_sup"]:
+        assert orc.kernel_error_sup(n, s, t) == v, (n, s, t)
+    linf, mse = orc.diff_stats(tools_golden["metric_a"], tools_golden["metric_b"])
+    assert linf == tools_scalars["metrics"]["linf"]
+    assert 10.0 * np.log10(mse) == tools_scalars["metrics"]["mse_db"]
+    q = orc.quantize_u8(tools_golden["io_edge_in"])
+    assert np.array_equal(q.ravel(), tools_golden["io_edge_pgm"][-q.size:])
