@@ -275,6 +275,7 @@ def main():
 
     # ---- this rank's share of the workload (host copies kept for e2e) --------------------
     bands = None
+    host_ext = None
     if cfg.batch > 1:
         idx = list(sharding.image_shard(cfg.batch, world, rank))
         host_imgs = [synth.config_image(cfg, i) for i in idx]
@@ -284,6 +285,8 @@ def main():
             bands = sharding.RowBands(cfg.height, world, W)
             r0, r1 = bands.bounds(rank)
             host_imgs = [np.ascontiguousarray(full[r0:r1])]
+            e0, e1 = bands.extended_bounds(rank)
+            host_ext = np.ascontiguousarray(full[e0:e1])  # the band with its halo rows (e2e leg)
         else:
             host_imgs = [full]
         del full
@@ -361,21 +364,31 @@ def main():
     # ---- e2e through the public API with host buffers ------------------------------------
     e2e = None
     if not args.no_e2e:
-        pinned_in = [torch.from_numpy(im).pin_memory().numpy() for im in host_imgs]
+        # row bands (N > 1): each rank's host input is its band plus the halo rows, filtered
+        # through the C ABI with halo_top / halo_bottom, so the band edges are exact
+        e2e_in = [host_ext] if host_ext is not None else host_imgs
+        pinned_in = [torch.from_numpy(im).pin_memory().numpy() for im in e2e_in]
         pinned_out = [torch.empty(im.shape, dtype=torch.float64).pin_memory().numpy() for im in host_imgs]
 
         def e2e_step():
             if len(pinned_in) > 1:
                 gpa_filter_batch(pinned_in, kernel, cfg.sigma_r, N, precision="f32", device=local, outs=pinned_out)
             else:
-                gpa_filter(pinned_in[0], kernel, cfg.sigma_r, N, precision="f32", device=local, out=pinned_out[0])
+                if host_ext is not None:
+                    top, bottom = bands.halos(rank)
+                    _native.gpa(pinned_in[0], pinned_out[0], kernel, cfg.sigma_r, N, 128.0, 128.0,
+                                _native.FB_PREC_F32, local, halo_top=top, halo_bottom=bottom)
+                else:
+                    gpa_filter(pinned_in[0], kernel, cfg.sigma_r, N, precision="f32", device=local,
+                               out=pinned_out[0])
 
-        e2e_step()
+        for _ in range(max(1, args.warmup)):  # the device leg's warm-up (small calls turn into
+            e2e_step()                         # CUDA-graph replays after the first sightings)
         if world > 1:
             dist.barrier()
         # Each call is synchronous (H2D, kernels, D2H on the context stream), so the
         # host clock around the calls is the end-to-end time.
-        n_e2e = max(1, min(args.steps, 3))
+        n_e2e = max(1, args.steps)
         t0 = time.perf_counter()
         for _ in range(n_e2e):
             e2e_step()
@@ -389,8 +402,8 @@ def main():
                "path": ("gpa_filter_batch" if len(pinned_in) > 1 else "gpa_filter")
                + "(pinned float32 numpy in, out= pinned float64 numpy): H2D, kernels and D2H pipelined on "
                  "three streams inside the call"
-               + ("; at N>1 each rank filters its own band (halo rows replicated at band edges in this leg)"
-                  if bands is not None else "")}
+               + ("; at N>1 each rank filters its band from host memory through fb_gpa_filter with its "
+                  "halo rows (libfbgpu C ABI), output rows to its own pinned buffer" if bands is not None else "")}
 
     if peer is not None:
         dist.barrier()  # every rank is done writing into the root's buffer before unmapping

@@ -120,6 +120,7 @@ struct fb_ctx {
     long long launches = 0;  // kernels in the graph (for fb_launch_count)
     int kev_used = 0;        // per-band timing events it records
     int bands = 0;           // row bands it runs (stats)
+    long long h2d = 0, d2h = 0;  // bytes its copies move (stats)
   };
   std::unordered_map<std::string, Graph> graphs;
   bool use_graphs = true;
@@ -395,8 +396,12 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
   bool any_host = false;  // the copy streams join only when some image lives in host memory
   for (auto& it : items) any_host |= !it.in->on_device || (it.out && !it.out->on_device);
   if (any_host) {
-    FB_CUDA(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_start, 0));
-    FB_CUDA(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_start, 0));
+    // fork the copy streams from the compute stream (an event recorded here, so a stream capture
+    // of this call takes them along)
+    cudaEvent_t fork = ctx->next_pev();
+    FB_CUDA(cudaEventRecord(fork, ctx->stream));
+    FB_CUDA(cudaStreamWaitEvent(ctx->s_h2d, fork, 0));
+    FB_CUDA(cudaStreamWaitEvent(ctx->s_d2h, fork, 0));
   }
   std::vector<cudaEvent_t> img_done(items.size(), nullptr);  // compute finished with image i's buffers
   std::vector<cudaEvent_t> out_done(items.size(), nullptr);  // D2H of image i finished
@@ -546,7 +551,8 @@ std::string graph_key(const fb_ctx* ctx, const fb_image* ins, const fb_image* ou
   const double dbl[] = {j.sr, j.tc, j.lo, j.hi};
   put(dbl, sizeof(dbl));
   if (j.taps) put(j.taps, sizeof(double) * (2 * j.W + 1));
-  const void* ptrs[] = {ctx->stream, ctx->ws, ctx->ws2, ctx->flags, ctx->tab, ctx->tabd};
+  const void* ptrs[] = {ctx->stream, ctx->ws,          ctx->ws2,         ctx->flags,       ctx->tab,
+                        ctx->tabd,   ctx->in_stage[0], ctx->in_stage[1], ctx->out_stage[0], ctx->out_stage[1]};
   put(ptrs, sizeof(ptrs));
   put(&ctx->ws_limit, sizeof(ctx->ws_limit));
   return k;
@@ -595,14 +601,27 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
                             ctx->stream));
     return FB_OK;
   };
-  // Small device-resident calls repeat with identical pointers and parameters (a serving loop,
-  // the c0/c1 configs) and are launch-bound: replay them as one CUDA graph instead of ~10
-  // separate launches, copies and records.  Large calls stay eager (launch cost is noise there
+  // Small calls repeat with identical pointers and parameters (a serving loop, the c0/c1
+  // configs) and are launch-bound: replay them as one CUDA graph instead of ~10-20 separate
+  // launches, copies and records.  Large calls stay eager (launch cost is noise there
   // and their per-kernel times feed the roofline reports).
-  bool device_only = true;
-  for (auto& it : items) device_only &= it.in->on_device && (!it.out || it.out->on_device);
+  // Graph replay needs every buffer to stay valid and addressable by copy engines between calls:
+  // device memory, or page-locked host memory (a capture of a copy from pageable memory would
+  // bake in a staging step that the runtime does eagerly).  The constant tables must already
+  // hold this order (no upload inside a capture).
+  auto replayable = [](const fb_image* im) {
+    if (im->on_device) return true;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, im->data) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  bool replay_ok = ctx->use_graphs && pixels <= kGraphMaxPixels && (outs == nullptr || ctx->tab_n == j.N);
+  for (auto& it : items) replay_ok = replay_ok && replayable(it.in) && (!it.out || replayable(it.out));
   fb_ctx::Graph* g = nullptr;
-  if (device_only && ctx->use_graphs && pixels <= kGraphMaxPixels) {
+  if (replay_ok) {
     std::string key = graph_key(ctx, ins, outs, count, halo_top, halo_bottom, j, precision);
     auto f = ctx->graphs.find(key);
     if (f == ctx->graphs.end()) {
@@ -618,6 +637,8 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
     g_launches += g->launches;
     ctx->kev_used = 0;  // no per-kernel events inside graphs (record_timing)
     local.bands = g->bands;
+    local.h2d_bytes = g->h2d;
+    local.d2h_bytes = g->d2h;
   } else if (g) {
     // second sighting: capture the same work, instantiate, launch
     FB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
@@ -637,6 +658,8 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
     }
     g->launches = g_launches.load() - launches0;
     g->bands = local.bands;
+    g->h2d = local.h2d_bytes;
+    g->d2h = local.d2h_bytes;
     ctx->kev_used = 0;
     FB_CUDA(cudaGraphLaunch(g->exec, ctx->stream));
   } else {

@@ -113,6 +113,23 @@ def test_walker_band_partitions_agree():
     assert np.max(np.abs(out.cpu().numpy() - ref64[r0:r1])) <= 5e-4
 
 
+def test_host_band_with_halos_chunked():
+    """The multi-GPU e2e leg: a host-resident band plus halo rows, pipelined in row chunks through
+    fb_gpa_filter (H2D / kernels / D2H on three streams), equals the same rows of the whole image."""
+    img = synth.config_image("c4", height=4096, width=2048)
+    k = make_spatial_kernel("box", half_width=20)
+    N, W = 57, 20
+    full = gpa_filter(img, k, 25.0, N, precision="f32")
+    for r0, r1 in ((0, 2300), (1000, 3300), (1800, 4096)):
+        top, bottom = min(W, r0), min(W, 4096 - r1)
+        ext = np.ascontiguousarray(img[r0 - top:r1 + bottom])
+        out = np.empty((r1 - r0, img.shape[1]), dtype=np.float64)
+        st = _native.gpa(ext, out, k, 25.0, N, 128.0, 128.0, _native.FB_PREC_F32, 0, halo_top=top,
+                         halo_bottom=bottom)
+        assert st["h2d_bytes"] == ext.nbytes and st["d2h_bytes"] == out.nbytes
+        assert np.max(np.abs(out - full[r0:r1])) <= 5e-4, (r0, r1)  # walks restart at other rows
+
+
 @pytest.mark.parametrize("width", [128, 130, 131, 133, 1029])
 def test_fp32_output_vector_and_scalar_stores(width):
     """float32 outputs use 128-bit stores where the row segment is aligned and complete, scalar
@@ -210,3 +227,32 @@ def test_graph_replay_of_small_repeated_calls():
     from paper_1603_08109_b200 import RangeViolationError
     with pytest.raises(RangeViolationError, match=r"row=5, col=7"):
         _native.gpa(src, out, k, 40.0, 15, 128.0, 128.0, _native.FB_PREC_F32, 0)
+
+
+def test_graph_replay_of_pinned_host_calls():
+    """Small calls on page-locked host buffers replay as one CUDA graph too (H2D, kernels, D2H
+    and the flag readback captured): same outputs, new input contents honoured, copy byte
+    counts kept; pageable buffers stay eager and give the same result."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(9)
+    img = np.floor(rng.uniform(0.0, 256.0, (300, 280)))
+    k = make_spatial_kernel("box", half_width=5)
+    src = torch.from_numpy(img).pin_memory().numpy()
+    out = torch.empty(img.shape, dtype=torch.float64).pin_memory().numpy()
+    ref = orc.gpa(img, "box", 5, k.weights_1d, 50.0, 10)
+    stats = []
+    for _ in range(5):  # eager (x2: the staging buffers appear in the key), capture, replay, replay
+        st = _native.gpa(src, out, k, 50.0, 10, 128.0, 128.0, _native.FB_PREC_F32, 0)
+        assert np.max(np.abs(out - ref)) <= F32_TOL
+        assert st["h2d_bytes"] == src.nbytes and st["d2h_bytes"] == out.nbytes
+        stats.append(st)
+    assert stats[0]["k1_ms"] > 0 and stats[-1]["k1_ms"] == -1.0
+    img2 = np.floor(rng.uniform(0.0, 256.0, img.shape))
+    src[...] = img2
+    _native.gpa(src, out, k, 50.0, 10, 128.0, 128.0, _native.FB_PREC_F32, 0)
+    assert np.max(np.abs(out - orc.gpa(img2, "box", 5, k.weights_1d, 50.0, 10))) <= F32_TOL
+    pageable_out = np.empty_like(out)
+    for _ in range(3):
+        st = _native.gpa(img2.copy(), pageable_out, k, 50.0, 10, 128.0, 128.0, _native.FB_PREC_F32, 0)
+        assert st["k1_ms"] > 0  # never replayed
+    assert np.array_equal(pageable_out, out)
