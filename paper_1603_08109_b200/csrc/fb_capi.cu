@@ -124,7 +124,6 @@ struct fb_ctx {
   };
   std::unordered_map<std::string, Graph> graphs;
   bool use_graphs = true;
-  int band_streams = 2;  // FBGPU_BAND_STREAMS=1: run the bands of one image on one stream
   void clear_graphs() {
     for (auto& kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -193,8 +192,7 @@ int order_delta1(double sigma_r, double w0, double T) {
 
 // The precision-typed argument block: constants once per call, pointers per image.
 template <typename T>
-int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a, int* band_out,
-            bool* split_out = nullptr) {
+int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a, int* band_out) {
   memset(&a, 0, sizeof(a));
   a.W = j.W;
   a.N = j.N;
@@ -296,12 +294,6 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
   if (band < 64) band = 64;
   const long long rows_pad = (rows_out_max + 63) / 64 * 64;
   if (band > rows_pad) band = rows_pad;
-  if (split_out) {
-    // An image of several bands runs them on two streams with two workspaces of half the limit
-    // each (run_items): kernel 1 of band b+1 (HBM writes) overlaps kernel 2 of band b (reads).
-    *split_out = band < rows_pad && ctx->band_streams > 1;
-    if (*split_out) band = std::max(64ll, ctx->ws_limit / 2 / std::max(per_row, 1ll) / 64 * 64);
-  }
   a.rstride = (long long)(j.N + 1) * a.pitch;
   a.band_max = (int)band;
   int rc = grow(&ctx->ws, &ctx->ws_bytes, (size_t)band * a.rstride * sizeof(T));
@@ -381,20 +373,16 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
               fb_stats* st) {
   const bool validate_only = items[0].out == nullptr;
   int band = 0;
-  bool split_bands = false;
   GpaArgs<T> a;
   int rows_max = 0;
   for (auto& it : items) rows_max = std::max(rows_max, it.rows_out);
   if (!validate_only) {
-    // a single image that is not split into host row chunks may split its bands over two streams
-    const bool may_split = items.size() == 1 && items[0].chunks == 1;
-    int rc = prepare<T>(ctx, j, (int)items[0].in->cols, rows_max, a, &band, may_split ? &split_bands : nullptr);
+    int rc = prepare<T>(ctx, j, (int)items[0].in->cols, rows_max, a, &band);
     if (rc != FB_OK) return rc;
   }
   // Batches alternate images between two compute streams with two workspaces, so the kernels
-  // of image i+1 fill the tail waves of image i; a single image of several bands alternates
-  // its bands the same way.
-  const bool dual = !validate_only && (items.size() > 1 || split_bands);
+  // of image i+1 fill the tail waves of image i.
+  const bool dual = !validate_only && items.size() > 1;
   cudaStream_t cs[2] = {ctx->stream, dual ? ctx->s_alt : ctx->stream};
   T* wsp[2] = {a.v, a.v};
   if (dual) {
@@ -489,22 +477,7 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
         a.flags = ctx->flags + 4 * i;
         a.v = wsp[slot];
         int nb = 0;
-        int rc = FB_OK;
-        if (split_bands) {
-          cudaEvent_t ef = ctx->next_pev();  // the second stream starts after this image's copy-in
-          FB_CUDA(cudaEventRecord(ef, cstr));
-          FB_CUDA(cudaStreamWaitEvent(cs[1], ef, 0));
-          for (int b0 = r0, bi = 0; b0 < r1 && rc == FB_OK; b0 += band, ++bi, ++nb) {
-            a.v = wsp[bi & 1];
-            rc = launch_band<T>(ctx, cs[bi & 1], j.kind, a, b0, std::min(band, r1 - b0));
-          }
-          // the copy-out (host output) and the end of the call wait for both streams
-          cudaEvent_t ej = ctx->next_pev();
-          FB_CUDA(cudaEventRecord(ej, cs[1]));
-          FB_CUDA(cudaStreamWaitEvent(cstr, ej, 0));
-        } else {
-          rc = run_rows<T>(ctx, cstr, j.kind, a, band, r0, r1, &nb);
-        }
+        int rc = run_rows<T>(ctx, cstr, j.kind, a, band, r0, r1, &nb);
         if (rc != FB_OK) return rc;
         if (st) st->bands += nb;
       }
@@ -874,8 +847,6 @@ int fb_create(int device, fb_ctx** out) {
   c->ws_limit = std::min<long long>(16ll << 30, (long long)(free_b / 4));
   const char* ng = std::getenv("FBGPU_NO_GRAPHS");  // debugging: always launch eagerly
   c->use_graphs = !(ng && *ng && *ng != '0');
-  const char* bs = std::getenv("FBGPU_BAND_STREAMS");
-  if (bs && *bs) c->band_streams = std::max(1, atoi(bs));
   *out = c;
   return FB_OK;
 }
