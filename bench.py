@@ -383,12 +383,18 @@ def main():
                                out=pinned_out[0])
 
         for _ in range(max(1, args.warmup)):  # the device leg's warm-up (small calls turn into
-            e2e_step()                         # CUDA-graph replays after the first sightings)
+            t_w = time.perf_counter()          # CUDA-graph replays after the first sightings)
+            e2e_step()
+            t_w = time.perf_counter() - t_w
+        # at least K calls, and enough of them to span ~0.2 s of host clock (sub-ms calls)
+        n_e2e = max(1, args.steps, min(4000, int(0.2 / max(t_w, 1e-6))))
         if world > 1:
+            n_t = torch.tensor([n_e2e], dtype=torch.int64, device=dev)
+            dist.all_reduce(n_t, op=dist.ReduceOp.MAX)
+            n_e2e = int(n_t.item())
             dist.barrier()
         # Each call is synchronous (H2D, kernels, D2H on the context stream), so the
         # host clock around the calls is the end-to-end time.
-        n_e2e = max(1, args.steps)
         t0 = time.perf_counter()
         for _ in range(n_e2e):
             e2e_step()

@@ -220,3 +220,21 @@ def test_bench_report(runner, pgm, tmp_path):
     r = json.loads(rep.read_text())
     assert all(v > 0 for v in r["runtime_ms"].values()) and r["params"]["repeats"] == 2
     assert set(r["runtime_ms"]) == {"gpa_box_W1_N2", "gpa_box_W1_N4", "gpa_box_W2_N2"}
+
+
+@pytest.mark.gpu
+def test_filter_png_roundtrip_and_report_bytes(runner, tmp_path, tools_golden):
+    """PNG in, PNG out through the uint8 path; the report's gpu block shows 1 byte per pixel each way."""
+    from paper_1603_08109_b200 import gpa_filter, make_spatial_kernel, read_raster, write_raster
+    src = tmp_path / "src.pgm"
+    src.write_bytes(tools_golden["cli_big"].tobytes())
+    raster = read_raster(src)
+    png_in, png_out, rep = tmp_path / "in.png", tmp_path / "out.png", tmp_path / "r.json"
+    write_raster(png_in, raster)
+    res = runner.invoke(main, ["filter", str(png_in), str(png_out), "--spatial", "box", "--window", "5",
+                               "--sigma-r", "30", "--order", "41", "--report", str(rep)])
+    assert res.exit_code == 0, res.output
+    r = json.loads(rep.read_text())
+    assert r["gpu"]["h2d_bytes"] == raster.size and r["gpu"]["d2h_bytes"] == raster.size
+    expect = gpa_filter(raster, make_spatial_kernel("box", half_width=5), 30.0, 41, out_dtype=np.uint8)
+    assert np.array_equal(read_raster(png_out), expect)
