@@ -10,6 +10,15 @@ exact filter, error metrology (`analysis`), PGM/PNG I/O and the CLI (`cli`).  Fi
 no CPU fallback.
 """
 
+import os as _os
+
+# FASTBILATERAL_THREADS caps the host's numeric thread pools (numpy/BLAS in the host-side helpers)
+# before numpy is first imported, as the reference package does (fastbilateral/__init__.py:10-16).
+_threads = _os.environ.get("FASTBILATERAL_THREADS")
+if _threads:
+    for _name in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        _os.environ.setdefault(_name, _threads)
+
 from .analysis import (ErrorReport, accuracy_bound, error_report, kernel_error_sup, linf_error, mse_db,
                        psi_eval)
 from .conv import apply_spatial, box_filter, convolve_direct, gaussian_filter

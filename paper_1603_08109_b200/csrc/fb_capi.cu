@@ -845,6 +845,8 @@ int fb_create(int device, fb_ctx** out) {
   size_t free_b = 0, total_b = 0;
   cudaMemGetInfo(&free_b, &total_b);
   c->ws_limit = std::min<long long>(16ll << 30, (long long)(free_b / 4));
+  const char* wl = std::getenv("FBGPU_WORKSPACE_GB");  // override the plane-workspace limit (GiB)
+  if (wl && *wl && atof(wl) > 0) c->ws_limit = (long long)(atof(wl) * (1ll << 30));
   const char* ng = std::getenv("FBGPU_NO_GRAPHS");  // debugging: always launch eagerly
   c->use_graphs = !(ng && *ng && *ng != '0');
   *out = c;
