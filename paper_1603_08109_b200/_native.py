@@ -184,10 +184,22 @@ def ipc_close(base: int) -> None:
     _check(lib, lib.fb_ipc_close(ctypes.c_void_p(base)), None, None)
 
 
+_spatial_cache: dict[int, tuple] = {}
+
+
 def spatial_desc(kernel):
+    """(FbSpatial, taps array keeping its pointer alive), cached per kernel object: the kernel is
+    frozen, and rebuilding the ctypes descriptor is a measurable part of a small call."""
+    hit = _spatial_cache.get(id(kernel))
+    if hit is not None and hit[0] is kernel:
+        return hit[1], hit[2]
     taps = np.ascontiguousarray(kernel.weights_1d, dtype=np.float64)
     kind = FB_BOX if kernel.kind == "box" else FB_GAUSSIAN
-    return FbSpatial(kind, int(kernel.half_width), taps.ctypes.data_as(ctypes.POINTER(ctypes.c_double))), taps
+    desc = FbSpatial(kind, int(kernel.half_width), taps.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    if len(_spatial_cache) >= 64:
+        _spatial_cache.clear()
+    _spatial_cache[id(kernel)] = (kernel, desc, taps)  # holds the kernel, so its id stays unique
+    return desc, taps
 
 
 def _check(lib, rc: int, src, stats: FbStats | None, lo=None, hi=None):
@@ -208,11 +220,30 @@ def _check(lib, rc: int, src, stats: FbStats | None, lo=None, hi=None):
     raise NativeError(f"libfbgpu: {msg} (status {rc})")
 
 
-def _stream_for(arr, device: int):
-    if is_cuda_tensor(arr):
+_raw_stream = None
+_last_stream: dict[int, int | None] = {}  # context address -> stream last bound with fb_set_stream
+
+
+def _stream_for(arr, device: int) -> int | None:
+    """Raw cudaStream_t of torch's current stream on the tensor's device (None: the context's own)."""
+    global _raw_stream
+    if not is_cuda_tensor(arr):
+        return None
+    if _raw_stream is None:
         import torch
-        return ctypes.c_void_p(torch.cuda.current_stream(arr.device).cuda_stream)
-    return ctypes.c_void_p(None)
+        getter = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        _raw_stream = getter if getter is not None else (
+            lambda idx: torch.cuda.current_stream(idx).cuda_stream)
+    return _raw_stream(arr.device.index or 0)
+
+
+def _bind_stream(lib, ctx, stream: int | None) -> None:
+    """fb_set_stream only when the stream differs from the one this context last used
+    (small repeated calls are launch-bound: every skipped ctypes call is latency)."""
+    key = ctx.value
+    if _last_stream.get(key, -1) != stream:
+        lib.fb_set_stream(ctx, ctypes.c_void_p(stream))
+        _last_stream[key] = stream
 
 
 def device_of(arr, device: int | None) -> int:
@@ -226,7 +257,7 @@ def gpa(src, out, kernel, sigma_r: float, order: int, center: float, half_range:
     """Run fb_gpa_filter; `src`/`out` are numpy arrays or CUDA tensors. Returns the stats dict."""
     lib = load_library()
     ctx = context(device)
-    lib.fb_set_stream(ctx, _stream_for(src, device))
+    _bind_stream(lib, ctx, _stream_for(src, device))
     sp, _taps = spatial_desc(kernel)
     st = FbStats()
     rc = lib.fb_gpa_filter(ctx, ctypes.byref(image_desc(src)), halo_top, halo_bottom, ctypes.byref(image_desc(out)),
@@ -241,7 +272,7 @@ def gpa_batch(srcs, outs, kernel, sigma_r: float, order: int, center: float, hal
     """Run fb_gpa_filter_batch over equally wide images (numpy arrays or CUDA tensors)."""
     lib = load_library()
     ctx = context(device)
-    lib.fb_set_stream(ctx, _stream_for(srcs[0], device))
+    _bind_stream(lib, ctx, _stream_for(srcs[0], device))
     sp, _taps = spatial_desc(kernel)
     n = len(srcs)
     ins = (FbImage * n)(*[image_desc(s) for s in srcs])
@@ -257,7 +288,7 @@ def gpa_batch(srcs, outs, kernel, sigma_r: float, order: int, center: float, hal
 def spatial(src, out, kernel, precision: int, device: int = 0) -> dict:
     lib = load_library()
     ctx = context(device)
-    lib.fb_set_stream(ctx, _stream_for(src, device))
+    _bind_stream(lib, ctx, _stream_for(src, device))
     sp, _taps = spatial_desc(kernel)
     st = FbStats()
     rc = lib.fb_spatial_filter(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)), ctypes.byref(sp),
@@ -269,7 +300,7 @@ def spatial(src, out, kernel, precision: int, device: int = 0) -> dict:
 def bilateral_exact(src, out, kernel, sigma_r: float, device: int = 0) -> dict:
     lib = load_library()
     ctx = context(device)
-    lib.fb_set_stream(ctx, _stream_for(src, device))
+    _bind_stream(lib, ctx, _stream_for(src, device))
     sp, _taps = spatial_desc(kernel)
     st = FbStats()
     rc = lib.fb_bilateral_exact(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)), ctypes.byref(sp),
@@ -282,7 +313,7 @@ def validate(src, lo: float, hi: float, device: int = 0) -> None:
     """Device-side as_image finiteness + validate_range; raises like the reference."""
     lib = load_library()
     ctx = context(device)
-    lib.fb_set_stream(ctx, _stream_for(src, device))
+    _bind_stream(lib, ctx, _stream_for(src, device))
     st = FbStats()
     rc = lib.fb_validate(ctx, ctypes.byref(image_desc(src)), float(lo), float(hi), ctypes.byref(st))
     _check(lib, rc, src, st, lo, hi)
@@ -292,7 +323,7 @@ def convolve_direct(src, out, weights_2d: np.ndarray, half_width: int, device: i
     """fb_convolve_direct: the literal 2-D convolution with the (2W+1)^2 table (conv.py:83-96)."""
     lib = load_library()
     ctx = context(device)
-    lib.fb_set_stream(ctx, _stream_for(src, device))
+    _bind_stream(lib, ctx, _stream_for(src, device))
     w2 = np.ascontiguousarray(weights_2d, dtype=np.float64)
     st = FbStats()
     rc = lib.fb_convolve_direct(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)), int(half_width),
@@ -305,7 +336,7 @@ def error_stats(a, b, device: int = 0) -> tuple[float, float]:
     """fb_error_stats: (max |a - b|, sum (a - b)^2) in fp64 on the device (analysis.py:33-46)."""
     lib = load_library()
     ctx = context(device)
-    lib.fb_set_stream(ctx, _stream_for(a, device))
+    _bind_stream(lib, ctx, _stream_for(a, device))
     linf, ss = ctypes.c_double(0.0), ctypes.c_double(0.0)
     st = FbStats()
     rc = lib.fb_error_stats(ctx, ctypes.byref(image_desc(a)), ctypes.byref(image_desc(b)), ctypes.byref(linf),
@@ -318,7 +349,7 @@ def kernel_error_sup(order: int, sigma_r: float, half_range: float, device: int 
     """fb_kernel_error_sup: grid supremum of the kernel error (analysis.py:70-103)."""
     lib = load_library()
     ctx = context(device)
-    lib.fb_set_stream(ctx, ctypes.c_void_p(None))
+    _bind_stream(lib, ctx, None)
     sup = ctypes.c_double(0.0)
     rc = lib.fb_kernel_error_sup(ctx, int(order), float(sigma_r), float(half_range), ctypes.byref(sup))
     _check(lib, rc, None, None)
