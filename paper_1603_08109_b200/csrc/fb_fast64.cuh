@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(KD2_THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, KD2_WARPS);
+      mbar_init(empty + s, KIND == kKindBox ? KD2_WARPS * 32 : KD2_WARPS);
     }
     mbar_fence_init();
   }
@@ -292,9 +292,15 @@ __global__ void __launch_bounds__(KD2_THREADS, 1)
   constexpr bool kSmemWin = KIND == kKindGauss;
   double win[kSmemWin ? 2 : WIN];
   const double* wsm = nullptr;
+  // box: one arrive per lane (no reconvergence point; as in the fp32 kernel 2), Gaussian: the
+  // warp-level release after the pass
   auto release = [&](int it) {
-    __syncwarp();
-    mbar_arrive_if(empty + it % STAGES, lane == 0);
+    if constexpr (KIND == kKindBox) {
+      fast::mbar_arrive(empty + it % STAGES);
+    } else {
+      __syncwarp();
+      mbar_arrive_if(empty + it % STAGES, lane == 0);
+    }
   };
   auto load_window = [&](int it) {
     const int s = it % STAGES;
