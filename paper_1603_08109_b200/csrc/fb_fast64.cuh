@@ -227,18 +227,24 @@ __host__ __device__ constexpr int kd2_stride(int W) {
   if (((s / 2) & 1) == 0) s += 2;
   return s;
 }
-// ring depth: 3 stages (Gaussian, compute-bound) / up to 6 (box), within 227 KB
+// Box: the window sums read the stage directly (no 50-double register window), so two CTAs
+// share an SM (probe knob FB_KD2_BOX_STREAM).
+#ifndef FB_KD2_BOX_STREAM
+#define FB_KD2_BOX_STREAM 1  // c4 f64 k2 7.53 -> 6.55 ms (with the stage-release proxy fence)
+#endif
+template <int KIND> __host__ __device__ constexpr int kd2_ctas() { return KIND == kKindBox && FB_KD2_BOX_STREAM ? 2 : 1; }
+// ring depth: 3 stages (Gaussian, compute-bound) / up to 6 (box), within the SM's 227 KB
 template <int KIND, int WT> __host__ __device__ constexpr int kd2_stages() {
-  return (KIND == kKindGauss ? 3 : 6) <= (227 * 1024 - 1280) / (KD2_TH * kd2_stride(WT) * 8)
+  return (KIND == kKindGauss ? 3 : 6) <= (227 * 1024 / kd2_ctas<KIND>() - 1280) / (KD2_TH * kd2_stride(WT) * 8)
              ? (KIND == kKindGauss ? 3 : 6)
-             : (227 * 1024 - 1280) / (KD2_TH * kd2_stride(WT) * 8);
+             : (227 * 1024 / kd2_ctas<KIND>() - 1280) / (KD2_TH * kd2_stride(WT) * 8);
 }
 inline size_t kd2_smem_bytes(int W, int stages) {
   return (size_t)stages * KD2_TH * kd2_stride(W) * sizeof(double) + 1024 + 2 * stages * 8;
 }
 
 template <int KIND, int WT>
-__global__ void __launch_bounds__(KD2_THREADS, 1)
+__global__ void __launch_bounds__(KD2_THREADS, kd2_ctas<KIND>())
     k2d_hpass_horner(const __grid_constant__ GpaArgs<double> a, const __grid_constant__ CUtensorMap planes) {
   extern __shared__ __align__(1024) double kd2_smem[];
   constexpr int STAGES = kd2_stages<KIND, WT>();
@@ -289,12 +295,14 @@ __global__ void __launch_bounds__(KD2_THREADS, 1)
   // Box windows (<= 72 doubles) are copied to registers and the stage released at once; the
   // Gaussian reads its taps' inputs straight from shared memory (its 8 x (2W+1) DFMAs would not
   // fit a register window) and releases the stage after the horizontal pass.
-  constexpr bool kSmemWin = KIND == kKindGauss;
+  constexpr bool kSmemWin = KIND == kKindGauss || FB_KD2_BOX_STREAM;
   double win[kSmemWin ? 2 : WIN];
   const double* wsm = nullptr;
   // box: one arrive per lane (no reconvergence point; as in the fp32 kernel 2), Gaussian: the
   // warp-level release after the pass
+  // (the proxy fence of fb_fast.cuh's kernel 2: stage reads ordered before the refill TMA)
   auto release = [&](int it) {
+    if constexpr (FB_K2_PROXY_FENCE) fast::fence_proxy_async_smem();
     if constexpr (KIND == kKindBox) {
       fast::mbar_arrive(empty + it % STAGES);
     } else {
@@ -336,6 +344,27 @@ __global__ void __launch_bounds__(KD2_THREADS, 1)
           const int k = m - j;
           if (k >= 0 && k <= 2 * WT) hv[j] = fma(a.w[k], c, hv[j]);
         }
+      }
+      release(it);
+    } else if constexpr (kSmemWin) {
+      // same sums, the window read from the stage two doubles at a time as it is reached
+      double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int q = 0; q < (2 * WT + 2) / 2; ++q) {
+        const double2 v = *reinterpret_cast<const double2*>(wsm + 2 * q);
+        if (2 * q <= 2 * WT) s4[(2 * q) & 3] += v.x;
+        if (2 * q + 1 <= 2 * WT) s4[(2 * q + 1) & 3] += v.y;
+      }
+      double sum = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+      hv[0] = sum;
+      double2 lv = make_double2(0.0, 0.0), ev = lv;
+#pragma unroll
+      for (int j = 1; j < KD2_R; ++j) {
+        const int il = j - 1, ie = j + 2 * WT;
+        if (j == 1 || (il & 1) == 0) lv = *reinterpret_cast<const double2*>(wsm + (il & ~1));
+        if (j == 1 || (ie & 1) == 0) ev = *reinterpret_cast<const double2*>(wsm + (ie & ~1));
+        sum += ((ie & 1) ? ev.y : ev.x) - ((il & 1) ? lv.y : lv.x);
+        hv[j] = sum;
       }
       release(it);
     } else {
