@@ -81,7 +81,7 @@ typedef struct fb_stats {
   int64_t order;                /* N */
   int64_t degenerate_pixels;    /* pixels that hit the |Q| < 1e-30 pass-through (engine.py:68-72) */
   int64_t nonfinite_outputs;    /* non-finite outputs (-> FB_ERR_NUMERIC) */
-  int64_t bad_index;            /* row-major index (in the input buffer) of the first offending sample */
+  int64_t bad_index;            /* row-major index (in the input buffer; fb_gpa_filter_band: in `in`) of the first offending sample */
   double bad_value;             /* its value */
   double device_ms;             /* device time of the whole call (CUDA events), incl. copies */
   double kernel_ms;             /* device time of the filter kernels only */
@@ -101,7 +101,10 @@ typedef struct fb_stats {
  * "allocated once" workspace of SPEC.md:383 lives). */
 int fb_create(int device, fb_ctx** out);
 int fb_destroy(fb_ctx* ctx);
-/* Use an existing cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL = the context's own. */
+/* Use an existing cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream); NULL = the context's own.
+ * cudaStreamLegacy / cudaStreamPerThread (a default stream; torch's default stream is the legacy one)
+ * run the work on the context's own stream, ordered after everything already queued on that default
+ * stream at each call (default streams cannot be captured into the CUDA graphs small calls replay). */
 int fb_set_stream(fb_ctx* ctx, void* cuda_stream);
 /* Upper bound for the channel-plane workspace (bytes); the image is processed in row bands below it. */
 int fb_set_workspace_limit(fb_ctx* ctx, int64_t bytes);
@@ -117,9 +120,12 @@ int fb_set_workspace_limit(fb_ctx* ctx, int64_t bytes);
  * buffer are replicated from its first/last row (the reference's edge pad).
  * Only the output rows are checked for finiteness / range [center -
  * half_range, center + half_range] (image.py:35-54).
- * Host-resident images of more than 4 MP are processed in 8 row chunks whose
- * copy-in, kernels and copy-out overlap on three streams (pinned host memory
- * makes the copies asynchronous; pageable memory still works, serialised).
+ * Host-resident images of more than 4 MP are processed in row chunks (8-64,
+ * multiples of 256 rows) whose copy-in, kernels and copy-out overlap on three
+ * streams (pinned host memory makes the copies asynchronous; pageable memory
+ * still works, serialised).  The result does not depend on the chunking, the
+ * workspace banding or the stream: every output is bit-identical to the one a
+ * single device-resident call computes.
  * `out` may be FB_F64 (the reference's float64 result), FB_F32, or FB_U8: the 8-bit raster that
  * save_pgm / save_image write (image.py:96-99, :122-127), quantised as floor(clip(v, 0, 255) + 0.5)
  * in kernel 2's epilogue, so a PGM/PNG pipeline moves 1 byte per pixel each way.
@@ -129,6 +135,26 @@ int fb_set_workspace_limit(fb_ctx* ctx, int64_t bytes);
 int fb_gpa_filter(fb_ctx* ctx, const fb_image* in, int64_t halo_top, int64_t halo_bottom,
                   fb_image* out, const fb_spatial* spatial, double sigma_r, int32_t order,
                   double center, double half_range, int32_t precision, fb_stats* stats);
+
+/*
+ * fb_gpa_filter_band — gpa_filter (engine.py:27-80) restricted to one row band of a larger
+ * image, for the row-band partitioning across GPUs (north star item 5, config c4).  `in` holds
+ * the band's own rows: image rows [row_origin, row_origin + in->rows) of an image_rows-row image.
+ * `above` / `below` (optional) are the rows just above / below the band (at most W are read),
+ * typically a row slice of a neighbour rank's band mapped with fb_ipc_open: kernel 1 reads them
+ * in place over NVLink / NVSwitch, so no halo exchange and no copy of the band is needed.  Rows
+ * beyond them are replicated (the reference's edge pad at the true image edges).  Halos in
+ * separate buffers must be device-resident, like `in`; halos that are the rows adjacent to `in`
+ * in its own buffer (same ld) may also be host memory (pipelined like fb_gpa_filter).
+ * The result is bit-identical to the same rows of one fb_gpa_filter call over the whole image
+ * when the halos hold W rows (or reach the image edge) and row_origin is a multiple of 256
+ * (box walks start at multiples of 256 image rows; a band starting elsewhere re-walks the rows
+ * above it, which need that many halo rows).  The box window check uses the whole image.
+ */
+int fb_gpa_filter_band(fb_ctx* ctx, const fb_image* in, const fb_image* above, const fb_image* below,
+                       int64_t row_origin, int64_t image_rows, fb_image* out, const fb_spatial* spatial,
+                       double sigma_r, int32_t order, double center, double half_range, int32_t precision,
+                       fb_stats* stats);
 
 /*
  * fb_gpa_filter_batch — the by-image partitioning of a batch (config c3):
@@ -211,6 +237,9 @@ int fb_ipc_close(void* base);
 /* Message of the last failure on this host thread. */
 const char* fb_last_error(void);
 int fb_version(void);
+/* Hash (16 hex digits) of the sources and compile flags this library was built from; the Python
+ * loader refuses a library whose id differs from the sources next to it (stale build). */
+const char* fb_build_id(void);
 /* Number of kernels this library has launched in this process (for launch accounting). */
 int64_t fb_launch_count(void);
 

@@ -30,7 +30,7 @@ EXPORTED_SYMBOLS = (
     "fb_create", "fb_destroy", "fb_set_stream", "fb_set_workspace_limit", "fb_gpa_filter",
     "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate", "fb_bilateral_exact", "fb_last_error",
     "fb_version", "fb_launch_count", "fb_ipc_export", "fb_ipc_open", "fb_ipc_close", "fb_convolve_direct",
-    "fb_error_stats", "fb_kernel_error_sup",
+    "fb_error_stats", "fb_kernel_error_sup", "fb_build_id", "fb_gpa_filter_band",
 )
 
 
@@ -61,6 +61,9 @@ class FbStats(ctypes.Structure):
 _lib = None
 _lib_lock = threading.Lock()
 _contexts: dict[int, ctypes.c_void_p] = {}
+# One lock per device context: a context (its workspace, flags, graphs) is not re-entrant
+# (fbgpu.h), while ctypes releases the GIL during every call.
+_ctx_locks: dict[int, threading.Lock] = {}
 
 
 def load_library(path: str | None = None) -> ctypes.CDLL:
@@ -88,6 +91,9 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
         lib.fb_gpa_filter.argtypes = [vp, P(FbImage), ctypes.c_int64, ctypes.c_int64, P(FbImage), P(FbSpatial),
                                       ctypes.c_double, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
                                       ctypes.c_int32, P(FbStats)]
+        lib.fb_gpa_filter_band.argtypes = [vp, P(FbImage), P(FbImage), P(FbImage), ctypes.c_int64, ctypes.c_int64,
+                                           P(FbImage), P(FbSpatial), ctypes.c_double, ctypes.c_int32,
+                                           ctypes.c_double, ctypes.c_double, ctypes.c_int32, P(FbStats)]
         lib.fb_gpa_filter_batch.argtypes = [vp, P(FbImage), P(FbImage), ctypes.c_int32, P(FbSpatial),
                                             ctypes.c_double, ctypes.c_int32, ctypes.c_double, ctypes.c_double,
                                             ctypes.c_int32, P(FbStats)]
@@ -102,9 +108,17 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
                                             P(ctypes.c_double)]
         lib.fb_last_error.restype = ctypes.c_char_p
         lib.fb_version.restype = ctypes.c_int
+        lib.fb_build_id.restype = ctypes.c_char_p
+        if path == LIB_PATH:
+            # the in-tree library must match the sources next to it (explicit paths are A/B variants)
+            from ._buildid import source_build_id
+            want, have = source_build_id(), lib.fb_build_id().decode()
+            if want is not None and have != want:
+                raise NativeError(f"{path} was built from other sources (build id {have}, sources {want}): "
+                                  "rebuild with __graft_entry__.build()")
         lib.fb_launch_count.restype = ctypes.c_int64
         for name in ("fb_create", "fb_destroy", "fb_set_stream", "fb_set_workspace_limit", "fb_gpa_filter",
-                     "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate", "fb_bilateral_exact",
+                     "fb_gpa_filter_band", "fb_gpa_filter_batch", "fb_spatial_filter", "fb_validate", "fb_bilateral_exact",
                      "fb_convolve_direct", "fb_error_stats", "fb_kernel_error_sup"):
             getattr(lib, name).restype = ctypes.c_int
         _lib = lib
@@ -122,7 +136,14 @@ def context(device: int = 0) -> ctypes.c_void_p:
             if rc != FB_OK:
                 raise NativeError(f"fb_create(device={device}) failed: {lib.fb_last_error().decode()}")
             _contexts[device] = ctx
+            _ctx_locks[device] = threading.Lock()
         return ctx
+
+
+def ctx_lock(device: int = 0) -> threading.Lock:
+    """The lock serialising calls into the context of `device` (held around bind + call)."""
+    context(device)
+    return _ctx_locks[device]
 
 
 def launch_count() -> int:
@@ -131,7 +152,10 @@ def launch_count() -> int:
 
 def set_workspace_limit(nbytes: int, device: int = 0) -> None:
     lib = load_library()
-    _check(lib, lib.fb_set_workspace_limit(context(device), int(nbytes)), None, None)
+    ctx = context(device)
+    with _ctx_locks[device]:
+        rc = lib.fb_set_workspace_limit(ctx, int(nbytes))
+    _check(lib, rc, None, None)
 
 
 # ----------------------------------------------------------------------------- arrays
@@ -221,6 +245,7 @@ def _check(lib, rc: int, src, stats: FbStats | None, lo=None, hi=None):
 
 
 _raw_stream = None
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy (cuda_runtime_api.h)
 _last_stream: dict[int, int | None] = {}  # context address -> stream last bound with fb_set_stream
 
 
@@ -234,7 +259,10 @@ def _stream_for(arr, device: int) -> int | None:
         getter = getattr(torch._C, "_cuda_getCurrentRawStream", None)
         _raw_stream = getter if getter is not None else (
             lambda idx: torch.cuda.current_stream(idx).cuda_stream)
-    return _raw_stream(arr.device.index or 0)
+    s = _raw_stream(arr.device.index or 0)
+    # torch's default stream is the legacy default stream (raw handle 0): bind it as
+    # cudaStreamLegacy so the library orders its work after what torch queued there
+    return CUDA_STREAM_LEGACY if not s else s
 
 
 def _bind_stream(lib, ctx, stream: int | None) -> None:
@@ -257,12 +285,34 @@ def gpa(src, out, kernel, sigma_r: float, order: int, center: float, half_range:
     """Run fb_gpa_filter; `src`/`out` are numpy arrays or CUDA tensors. Returns the stats dict."""
     lib = load_library()
     ctx = context(device)
-    _bind_stream(lib, ctx, _stream_for(src, device))
     sp, _taps = spatial_desc(kernel)
     st = FbStats()
-    rc = lib.fb_gpa_filter(ctx, ctypes.byref(image_desc(src)), halo_top, halo_bottom, ctypes.byref(image_desc(out)),
-                           ctypes.byref(sp), float(sigma_r), int(order), float(center), float(half_range),
-                           int(precision), ctypes.byref(st))
+    with _ctx_locks[device]:
+        _bind_stream(lib, ctx, _stream_for(src, device))
+        rc = lib.fb_gpa_filter(ctx, ctypes.byref(image_desc(src)), halo_top, halo_bottom,
+                               ctypes.byref(image_desc(out)), ctypes.byref(sp), float(sigma_r), int(order),
+                               float(center), float(half_range), int(precision), ctypes.byref(st))
+    _check(lib, rc, src, st, center - half_range, center + half_range)
+    return st.as_dict()
+
+
+def gpa_band(src, out, kernel, sigma_r: float, order: int, center: float, half_range: float, precision: int,
+             row_origin: int, image_rows: int, above=None, below=None, device: int = 0) -> dict:
+    """Run fb_gpa_filter_band: `src` = rows [row_origin, row_origin + rows) of an image_rows-row image,
+    `above` / `below` = the neighbouring rows (CUDA tensors or FbImage views of a peer's buffer)."""
+    lib = load_library()
+    ctx = context(device)
+    sp, _taps = spatial_desc(kernel)
+    st = FbStats()
+    ab = image_desc(above) if above is not None else None
+    be = image_desc(below) if below is not None else None
+    with _ctx_locks[device]:
+        _bind_stream(lib, ctx, _stream_for(src, device))
+        rc = lib.fb_gpa_filter_band(ctx, ctypes.byref(image_desc(src)), ctypes.byref(ab) if ab is not None else None,
+                                    ctypes.byref(be) if be is not None else None, int(row_origin),
+                                    int(image_rows), ctypes.byref(image_desc(out)), ctypes.byref(sp),
+                                    float(sigma_r), int(order), float(center), float(half_range), int(precision),
+                                    ctypes.byref(st))
     _check(lib, rc, src, st, center - half_range, center + half_range)
     return st.as_dict()
 
@@ -272,14 +322,15 @@ def gpa_batch(srcs, outs, kernel, sigma_r: float, order: int, center: float, hal
     """Run fb_gpa_filter_batch over equally wide images (numpy arrays or CUDA tensors)."""
     lib = load_library()
     ctx = context(device)
-    _bind_stream(lib, ctx, _stream_for(srcs[0], device))
     sp, _taps = spatial_desc(kernel)
     n = len(srcs)
     ins = (FbImage * n)(*[image_desc(s) for s in srcs])
     outs_d = (FbImage * n)(*[image_desc(o) for o in outs])
     st = FbStats()
-    rc = lib.fb_gpa_filter_batch(ctx, ins, outs_d, n, ctypes.byref(sp), float(sigma_r), int(order),
-                                 float(center), float(half_range), int(precision), ctypes.byref(st))
+    with _ctx_locks[device]:
+        _bind_stream(lib, ctx, _stream_for(srcs[0], device))
+        rc = lib.fb_gpa_filter_batch(ctx, ins, outs_d, n, ctypes.byref(sp), float(sigma_r), int(order),
+                                     float(center), float(half_range), int(precision), ctypes.byref(st))
     bad = srcs[st.bad_image] if st.bad_image >= 0 else srcs[0]
     _check(lib, rc, bad, st, center - half_range, center + half_range)
     return st.as_dict()
@@ -288,11 +339,12 @@ def gpa_batch(srcs, outs, kernel, sigma_r: float, order: int, center: float, hal
 def spatial(src, out, kernel, precision: int, device: int = 0) -> dict:
     lib = load_library()
     ctx = context(device)
-    _bind_stream(lib, ctx, _stream_for(src, device))
     sp, _taps = spatial_desc(kernel)
     st = FbStats()
-    rc = lib.fb_spatial_filter(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)), ctypes.byref(sp),
-                               int(precision), ctypes.byref(st))
+    with _ctx_locks[device]:
+        _bind_stream(lib, ctx, _stream_for(src, device))
+        rc = lib.fb_spatial_filter(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)),
+                                   ctypes.byref(sp), int(precision), ctypes.byref(st))
     _check(lib, rc, src, st)
     return st.as_dict()
 
@@ -300,11 +352,12 @@ def spatial(src, out, kernel, precision: int, device: int = 0) -> dict:
 def bilateral_exact(src, out, kernel, sigma_r: float, device: int = 0) -> dict:
     lib = load_library()
     ctx = context(device)
-    _bind_stream(lib, ctx, _stream_for(src, device))
     sp, _taps = spatial_desc(kernel)
     st = FbStats()
-    rc = lib.fb_bilateral_exact(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)), ctypes.byref(sp),
-                                float(sigma_r), ctypes.byref(st))
+    with _ctx_locks[device]:
+        _bind_stream(lib, ctx, _stream_for(src, device))
+        rc = lib.fb_bilateral_exact(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)),
+                                    ctypes.byref(sp), float(sigma_r), ctypes.byref(st))
     _check(lib, rc, src, st)
     return st.as_dict()
 
@@ -313,9 +366,10 @@ def validate(src, lo: float, hi: float, device: int = 0) -> None:
     """Device-side as_image finiteness + validate_range; raises like the reference."""
     lib = load_library()
     ctx = context(device)
-    _bind_stream(lib, ctx, _stream_for(src, device))
     st = FbStats()
-    rc = lib.fb_validate(ctx, ctypes.byref(image_desc(src)), float(lo), float(hi), ctypes.byref(st))
+    with _ctx_locks[device]:
+        _bind_stream(lib, ctx, _stream_for(src, device))
+        rc = lib.fb_validate(ctx, ctypes.byref(image_desc(src)), float(lo), float(hi), ctypes.byref(st))
     _check(lib, rc, src, st, lo, hi)
 
 
@@ -323,11 +377,13 @@ def convolve_direct(src, out, weights_2d: np.ndarray, half_width: int, device: i
     """fb_convolve_direct: the literal 2-D convolution with the (2W+1)^2 table (conv.py:83-96)."""
     lib = load_library()
     ctx = context(device)
-    _bind_stream(lib, ctx, _stream_for(src, device))
     w2 = np.ascontiguousarray(weights_2d, dtype=np.float64)
     st = FbStats()
-    rc = lib.fb_convolve_direct(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)), int(half_width),
-                                w2.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(st))
+    with _ctx_locks[device]:
+        _bind_stream(lib, ctx, _stream_for(src, device))
+        rc = lib.fb_convolve_direct(ctx, ctypes.byref(image_desc(src)), ctypes.byref(image_desc(out)),
+                                    int(half_width), w2.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                    ctypes.byref(st))
     _check(lib, rc, src, st)
     return st.as_dict()
 
@@ -336,11 +392,12 @@ def error_stats(a, b, device: int = 0) -> tuple[float, float]:
     """fb_error_stats: (max |a - b|, sum (a - b)^2) in fp64 on the device (analysis.py:33-46)."""
     lib = load_library()
     ctx = context(device)
-    _bind_stream(lib, ctx, _stream_for(a, device))
     linf, ss = ctypes.c_double(0.0), ctypes.c_double(0.0)
     st = FbStats()
-    rc = lib.fb_error_stats(ctx, ctypes.byref(image_desc(a)), ctypes.byref(image_desc(b)), ctypes.byref(linf),
-                            ctypes.byref(ss), ctypes.byref(st))
+    with _ctx_locks[device]:
+        _bind_stream(lib, ctx, _stream_for(a, device))
+        rc = lib.fb_error_stats(ctx, ctypes.byref(image_desc(a)), ctypes.byref(image_desc(b)), ctypes.byref(linf),
+                                ctypes.byref(ss), ctypes.byref(st))
     _check(lib, rc, a, st)
     return float(linf.value), float(ss.value)
 
@@ -349,8 +406,9 @@ def kernel_error_sup(order: int, sigma_r: float, half_range: float, device: int 
     """fb_kernel_error_sup: grid supremum of the kernel error (analysis.py:70-103)."""
     lib = load_library()
     ctx = context(device)
-    _bind_stream(lib, ctx, None)
     sup = ctypes.c_double(0.0)
-    rc = lib.fb_kernel_error_sup(ctx, int(order), float(sigma_r), float(half_range), ctypes.byref(sup))
+    with _ctx_locks[device]:
+        _bind_stream(lib, ctx, None)
+        rc = lib.fb_kernel_error_sup(ctx, int(order), float(sigma_r), float(half_range), ctypes.byref(sup))
     _check(lib, rc, None, None)
     return float(sup.value)

@@ -124,6 +124,13 @@ struct fb_ctx {
   };
   std::unordered_map<std::string, Graph> graphs;
   bool use_graphs = true;
+  // A buffer a captured graph may reference was freed and reallocated (grow, ensure_flags, the
+  // constant tables): every graph is dropped at the start of the next call (execute()).
+  bool realloc_seen = false;
+  // The caller's stream was the legacy (or per-thread) default stream, which cannot be captured
+  // into graphs: work runs on own_stream, ordered after everything already queued there.
+  cudaStream_t upstream = nullptr;
+  cudaEvent_t ev_upstream = nullptr;
   void clear_graphs() {
     for (auto& kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -144,8 +151,9 @@ struct fb_ctx {
 
 namespace {
 
-int grow(void** p, size_t* have, size_t need) {
+int grow(fb_ctx* ctx, void** p, size_t* have, size_t need) {
   if (*have >= need) return FB_OK;
+  ctx->realloc_seen = true;
   if (*p) cudaFree(*p);
   *p = nullptr;
   *have = 0;
@@ -177,19 +185,6 @@ struct Job {
   double sr, tc, lo, hi;
 };
 
-// Order that Algorithm 1 (order.py:91-153) selects for a per-pixel error of delta = 1 gray level:
-// the smallest N > lambda whose Chernoff bound meets eps = w0 / (2T + 1) (exhaustive scan; the
-// Lambert-W estimate agrees to +-1, tests/test_order.py).  Used only for the Horner-precision policy.
-int order_delta1(double sigma_r, double w0, double T) {
-  const double eps = w0 / (2.0 * T + 1.0);
-  const double lam = (T / sigma_r) * (T / sigma_r);
-  if (sigma_r >= 70.0) return 10;
-  if (!(eps > 0.0 && eps < 1.0)) return 0;
-  int n = (int)std::floor(lam) + 1;
-  while (n < 100000 && -lam + n * (1.0 + std::log(lam) - std::log((double)n)) > std::log(eps)) ++n;
-  return n;
-}
-
 // The precision-typed argument block: constants once per call, pointers per image.
 template <typename T>
 int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a, int* band_out) {
@@ -205,10 +200,6 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
   a.hi = j.hi;
   a.cols = cols;
   const int n_taps = 2 * j.W + 1;
-  {
-    const double w0 = j.kind == FB_BOX ? 1.0 / ((double)n_taps * n_taps) : j.taps[j.W] * j.taps[j.W];
-    a.n_delta1 = j.mode == kModeGpa ? order_delta1(j.sr, w0, (j.hi - j.lo) / 2.0) : 0;
-  }
   if (j.kind == FB_BOX) {
     a.norm = (T)(1.0 / ((double)n_taps * n_taps));
     for (int k = 0; k < n_taps; ++k) a.w[k] = T(1);
@@ -229,6 +220,7 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
     a.rsc2[2 * m] = a.rsc2[2 * m + 1] = walk_q(m);
   // channel constants 1/sqrt(m), sqrt(m) (rounded once from double), uploaded when N changes
   if (j.N + 1 > ctx->tab_cap) {
+    ctx->realloc_seen = true;
     for (void* p : {(void*)ctx->tab, (void*)ctx->tabd}) if (p) cudaFree(p);
     for (void* p : {(void*)ctx->tab_host, (void*)ctx->tabd_host}) if (p) cudaFreeHost(p);
     ctx->tab = nullptr;
@@ -289,14 +281,16 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
   a.pitch = (a.wpad + 31) / 32 * 32;
   // Row bands: the N+1 planes of one band must fit under the workspace limit.
   const long long per_row = (long long)(j.N + 1) * a.pitch * (long long)sizeof(T);
+  // Bands start at multiples of 256 image rows when they can (the box walks and tiles then
+  // start at the band's first row: no rows above it are walked, see walk_rows()).
   long long band = ctx->ws_limit / std::max(per_row, 1ll);
-  band = band / 64 * 64;
+  band = band >= 256 ? band / 256 * 256 : band / 64 * 64;
   if (band < 64) band = 64;
   const long long rows_pad = (rows_out_max + 63) / 64 * 64;
   if (band > rows_pad) band = rows_pad;
   a.rstride = (long long)(j.N + 1) * a.pitch;
   a.band_max = (int)band;
-  int rc = grow(&ctx->ws, &ctx->ws_bytes, (size_t)band * a.rstride * sizeof(T));
+  int rc = grow(ctx, &ctx->ws, &ctx->ws_bytes, (size_t)band * a.rstride * sizeof(T));
   if (rc != FB_OK) return rc;
   a.v = reinterpret_cast<T*>(ctx->ws);
   *band_out = (int)band;
@@ -319,7 +313,9 @@ int launch_band(fb_ctx* ctx, cudaStream_t st, int kind, GpaArgs<T>& a, int band_
     return FB_OK;
   }
   const size_t s1 = generic::k1_smem<T>(W), s2 = generic::k2_smem<T>(W);
-  dim3 g1((a.wpad + generic::K1_TC - 1) / generic::K1_TC, (band_rows + generic::K1_RB - 1) / generic::K1_RB);
+  a.lead = kind == FB_BOX ? box_lead(a, generic::K1_RB) : 0;
+  dim3 g1((a.wpad + generic::K1_TC - 1) / generic::K1_TC,
+          (band_rows + a.lead + generic::K1_RB - 1) / generic::K1_RB);
   dim3 g2((a.cols + generic::K2_TW - 1) / generic::K2_TW, (band_rows + generic::K2_TH - 1) / generic::K2_TH);
   auto k1 = kind == FB_BOX ? generic::k1_gen_vpass<T, kKindBox> : generic::k1_gen_vpass<T, kKindGauss>;
   auto k2 = kind == FB_BOX ? generic::k2_hpass_horner<T, kKindBox> : generic::k2_hpass_horner<T, kKindGauss>;
@@ -347,6 +343,16 @@ int run_rows(fb_ctx* ctx, cudaStream_t st, int kind, GpaArgs<T>& a, int band, in
   return FB_OK;
 }
 
+// Where the output rows of a call sit in the whole image, and where its halo rows come from.
+struct Geom {
+  long long row_origin = 0;         // image row of output row 0
+  long long image_rows = 0;         // rows of the whole image (0: the output rows are the image)
+  const fb_image* above = nullptr;  // halo rows in separate device buffers (fb_gpa_filter_band);
+  const fb_image* below = nullptr;  // else the halo rows are part of the input buffer
+  bool separate() const { return above != nullptr || below != nullptr; }
+  long long report_rows = 0;        // stats->bad_index counts rows from this many rows below the buffer start
+};
+
 // One image of a call: where its data lives on the device and how it is chunked.
 struct Item {
   const fb_image* in;
@@ -370,7 +376,7 @@ struct Item {
 // Kernels of a chunk wait for the input rows they read (chunk rows + W halo rows).
 template <typename T>
 int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bottom, const Job& j,
-              fb_stats* st) {
+              fb_stats* st, const Geom& geo) {
   const bool validate_only = items[0].out == nullptr;
   int band = 0;
   GpaArgs<T> a;
@@ -386,7 +392,7 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
   cudaStream_t cs[2] = {ctx->stream, dual ? ctx->s_alt : ctx->stream};
   T* wsp[2] = {a.v, a.v};
   if (dual) {
-    int rc = grow(&ctx->ws2, &ctx->ws2_bytes, (size_t)band * a.rstride * sizeof(T));
+    int rc = grow(ctx, &ctx->ws2, &ctx->ws2_bytes, (size_t)band * a.rstride * sizeof(T));
     if (rc != FB_OK) return rc;
     wsp[1] = reinterpret_cast<T*>(ctx->ws2);
     cudaEvent_t e = ctx->next_pev();  // after the constant-table upload in prepare()
@@ -415,7 +421,7 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
     const bool host_out = it.out && !it.out->on_device;
     // device buffers (double-buffered across images; reuse waits for image i-2)
     if (host_in) {
-      int rc = grow(&ctx->in_stage[slot], &ctx->in_stage_bytes[slot], (size_t)in->rows * in->cols * ies);
+      int rc = grow(ctx, &ctx->in_stage[slot], &ctx->in_stage_bytes[slot], (size_t)in->rows * in->cols * ies);
       if (rc != FB_OK) return rc;
       it.f = ctx->in_stage[slot];
       it.f_ld = in->cols;
@@ -427,7 +433,7 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
     if (it.out) {
       const size_t oes = dtype_size(it.out->dtype);
       if (host_out) {
-        int rc = grow(&ctx->out_stage[slot], &ctx->out_stage_bytes[slot], (size_t)it.rows_out * it.out->cols * oes);
+        int rc = grow(ctx, &ctx->out_stage[slot], &ctx->out_stage_bytes[slot], (size_t)it.rows_out * it.out->cols * oes);
         if (rc != FB_OK) return rc;
         it.o = ctx->out_stage[slot];
         it.o_ld = it.out->cols;
@@ -439,7 +445,8 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
     }
     const int W = validate_only ? 0 : j.W;
     const int nch = it.chunks;
-    const int crows = (it.rows_out + nch - 1) / nch;
+    int crows = (it.rows_out + nch - 1) / nch;
+    if (nch > 1) crows = (crows + 255) / 256 * 256;  // chunks start at multiples of 256 rows (walk_rows)
     long long copied = 0;  // input buffer rows already sent
     for (int c = 0; c < nch; ++c) {
       const int r0 = c * crows, r1 = std::min(it.rows_out, r0 + crows);
@@ -466,11 +473,30 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
         if (rc != FB_OK) return fail(FB_ERR_CUDA, "validation kernel launch failed");
         g_launches += 1;
       } else {
-        a.f = it.f;
         a.f_ld = it.f_ld;
         a.f_dtype = in->dtype;
-        a.rows_in = (int)in->rows;
         a.halo_top = halo_top;
+        a.rows_in = halo_top + it.rows_out + halo_bottom;
+        a.main_end = halo_top + it.rows_out;
+        a.row_origin = geo.row_origin;
+        a.image_rows = (int)(geo.image_rows > 0 ? geo.image_rows : it.rows_out);
+        if (geo.separate()) {
+          // own rows from `in`, halo rows from the neighbours' buffers: offsets relative to a
+          // virtual buffer row 0 that sits halo_top rows above in->data (never dereferenced)
+          const long long ies_l = (long long)ies;
+          const intptr_t f0 = reinterpret_cast<intptr_t>(it.f) - (intptr_t)halo_top * it.f_ld * ies_l;
+          a.f = reinterpret_cast<const void*>(f0);
+          a.top_off = geo.above ? (reinterpret_cast<intptr_t>(geo.above->data) - f0) / ies_l : 0;
+          a.top_ld = geo.above ? geo.above->ld : it.f_ld;
+          a.bot_off = geo.below ? (reinterpret_cast<intptr_t>(geo.below->data) - f0) / ies_l : 0;
+          a.bot_ld = geo.below ? geo.below->ld : it.f_ld;
+        } else {
+          a.f = it.f;
+          a.top_off = 0;
+          a.top_ld = it.f_ld;
+          a.bot_off = (long long)a.main_end * it.f_ld;
+          a.bot_ld = it.f_ld;
+        }
         a.out = it.o;
         a.out_ld = it.o_ld;
         a.out_dtype = it.out->dtype;
@@ -514,6 +540,7 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
 
 int ensure_flags(fb_ctx* ctx, int count) {
   if (count <= ctx->flags_cap) return FB_OK;
+  ctx->realloc_seen = true;
   if (ctx->flags) cudaFree(ctx->flags);
   if (ctx->flags_host) cudaFreeHost(ctx->flags_host);
   ctx->flags = nullptr;
@@ -533,13 +560,22 @@ int ensure_flags(fb_ctx* ctx, int count) {
   return FB_OK;
 }
 
+// The caller bound the legacy / per-thread default stream (fb_set_stream): order the context's
+// stream after the work already queued there (e.g. a torch kernel still writing the input).
+int order_after_caller(fb_ctx* ctx) {
+  if (!ctx->upstream) return FB_OK;
+  FB_CUDA(cudaEventRecord(ctx->ev_upstream, ctx->upstream));
+  FB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_upstream, 0));
+  return FB_OK;
+}
+
 // Run `count` images through the pipeline, read the flags back and map them to a status.
 constexpr long long kGraphMaxPixels = 16ll << 20;  // calls up to 16 MP run as CUDA graphs
 
 // Everything the GPU work of a device-resident call depends on: the images (pointers, shapes,
 // strides, dtypes), the filter (incl. taps), precision, halos, the stream and the workspaces.
 std::string graph_key(const fb_ctx* ctx, const fb_image* ins, const fb_image* outs, int count, int halo_top,
-                      int halo_bottom, const Job& j, int precision) {
+                      int halo_bottom, const Job& j, int precision, const Geom& geo) {
   std::string k;
   auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
   for (int i = 0; i < count; ++i) {
@@ -551,23 +587,34 @@ std::string graph_key(const fb_ctx* ctx, const fb_image* ins, const fb_image* ou
   const double dbl[] = {j.sr, j.tc, j.lo, j.hi};
   put(dbl, sizeof(dbl));
   if (j.taps) put(j.taps, sizeof(double) * (2 * j.W + 1));
-  const void* ptrs[] = {ctx->stream, ctx->ws,          ctx->ws2,         ctx->flags,       ctx->tab,
-                        ctx->tabd,   ctx->in_stage[0], ctx->in_stage[1], ctx->out_stage[0], ctx->out_stage[1]};
+  const void* ptrs[] = {ctx->stream,       ctx->ws,           ctx->ws2,         ctx->flags,
+                        ctx->flags_host,   ctx->tab,          ctx->tabd,        ctx->in_stage[0],
+                        ctx->in_stage[1],  ctx->out_stage[0], ctx->out_stage[1]};
   put(ptrs, sizeof(ptrs));
-  put(&ctx->ws_limit, sizeof(ctx->ws_limit));
+  const long long sizes[] = {ctx->ws_limit, ctx->flags_cap, ctx->tab_cap, geo.row_origin, geo.image_rows};
+  put(sizes, sizeof(sizes));
+  for (const fb_image* h : {geo.above, geo.below}) {
+    const fb_image none{};
+    put(h ? h : &none, sizeof(fb_image));
+  }
   return k;
 }
 
 int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int halo_top, int halo_bottom,
-            const Job& j, int precision, fb_stats* st) {
+            const Job& j, int precision, fb_stats* st, const Geom& geo = Geom()) {
   FB_CUDA(cudaSetDevice(ctx->device));
   fb_stats local;
   memset(&local, 0, sizeof(local));
   local.bad_image = -1;
   int rc = ensure_flags(ctx, count);
   if (rc != FB_OK) return rc;
+  if (ctx->realloc_seen) {  // a graph may reference a freed buffer
+    ctx->clear_graphs();
+    ctx->realloc_seen = false;
+  }
   ctx->kev_used = 0;
   ctx->pev_used = 0;
+  if ((rc = order_after_caller(ctx)) != FB_OK) return rc;
   FB_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
   std::vector<Item> items(count);
   long long pixels = 0;
@@ -576,7 +623,7 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
     memset(&it, 0, sizeof(it));
     it.in = ins + i;
     it.out = outs ? outs + i : nullptr;
-    it.rows_out = (int)(ins[i].rows - halo_top - halo_bottom);
+    it.rows_out = (int)(geo.separate() ? ins[i].rows : ins[i].rows - halo_top - halo_bottom);
     pixels += (long long)it.rows_out * ins[i].cols;
     // host images of more than 4 MP are pipelined in row chunks of ~FB_CHUNK_PX pixels (at least
     // 8 chunks, at most 64, >= 256 rows each): the un-overlapped first H2D and last D2H shrink
@@ -594,8 +641,8 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
   auto enqueue = [&]() -> int {
     FB_CUDA(cudaMemcpyAsync(ctx->flags, ctx->flags_host, 4 * sizeof(unsigned long long) * count,
                             cudaMemcpyHostToDevice, ctx->stream));
-    int r = precision == FB_PREC_F64 ? run_items<double>(ctx, items, halo_top, halo_bottom, j, &local)
-                                     : run_items<float>(ctx, items, halo_top, halo_bottom, j, &local);
+    int r = precision == FB_PREC_F64 ? run_items<double>(ctx, items, halo_top, halo_bottom, j, &local, geo)
+                                     : run_items<float>(ctx, items, halo_top, halo_bottom, j, &local, geo);
     if (r != FB_OK) return r;
     FB_CUDA(cudaMemcpyAsync(fl_all, ctx->flags, 4 * sizeof(unsigned long long) * count, cudaMemcpyDeviceToHost,
                             ctx->stream));
@@ -622,7 +669,7 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
   for (auto& it : items) replay_ok = replay_ok && replayable(it.in) && (!it.out || replayable(it.out));
   fb_ctx::Graph* g = nullptr;
   if (replay_ok) {
-    std::string key = graph_key(ctx, ins, outs, count, halo_top, halo_bottom, j, precision);
+    std::string key = graph_key(ctx, ins, outs, count, halo_top, halo_bottom, j, precision, geo);
     auto f = ctx->graphs.find(key);
     if (f == ctx->graphs.end()) {
       if (ctx->graphs.size() >= 16) ctx->clear_graphs();
@@ -675,8 +722,15 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
 
   int status = FB_OK;
   for (int i = 0; i < count && status == FB_OK; ++i) {
-    const unsigned long long* fl = fl_all + 4 * i;
+    unsigned long long fl[4];
+    memcpy(fl, fl_all + 4 * i, sizeof(fl));
     const fb_image* in = ins + i;
+    if (geo.separate()) {  // flagged indices count buffer rows from the virtual row 0 above `in`
+      for (int k : {kFlagFirstNonfinite, kFlagFirstRange})
+        if (fl[k] != ~0ull) fl[k] -= (unsigned long long)halo_top * in->cols;
+    }
+    // band calls report rows of the band itself
+    const long long report_shift = (geo.separate() ? 0 : geo.report_rows) * in->cols;
     const size_t ies = dtype_size(in->dtype);
     local.degenerate_pixels += (long long)fl[kFlagDegenerate];
     local.nonfinite_outputs += (long long)fl[kFlagNonfiniteOut];
@@ -694,12 +748,12 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
       double v; memcpy(&v, buf, 8); return v;
     };
     if (fl[kFlagFirstNonfinite] != ~0ull) {
-      local.bad_index = (long long)fl[kFlagFirstNonfinite];
+      local.bad_index = (long long)fl[kFlagFirstNonfinite] - report_shift;
       local.bad_value = sample_at(fl[kFlagFirstNonfinite]);
       local.bad_image = i;
       status = fail(FB_ERR_NONFINITE_INPUT, "image contains non-finite samples");
     } else if (fl[kFlagFirstRange] != ~0ull) {
-      local.bad_index = (long long)fl[kFlagFirstRange];
+      local.bad_index = (long long)fl[kFlagFirstRange] - report_shift;
       local.bad_value = sample_at(fl[kFlagFirstRange]);
       local.bad_image = i;
       status = fail(FB_ERR_RANGE, "sample outside the declared range");
@@ -817,6 +871,13 @@ int fb_ipc_close(void* base) {
   return FB_OK;
 }
 
+#ifndef FB_BUILD_ID
+#define FB_BUILD_ID "unknown"
+#endif
+// "FBGPU_BUILD_ID=<hash of the sources and flags>" stays in the binary's read-only data, so
+// build() can read it from the file and load_library() from fb_build_id().
+static const char kBuildId[] = "FBGPU_BUILD_ID=" FB_BUILD_ID;
+const char* fb_build_id(void) { return kBuildId + 15; }
 int fb_version(void) { return FBGPU_VERSION; }
 int64_t fb_launch_count(void) { return (int64_t)g_launches.load(); }
 const char* fb_last_error(void) { return g_last_error.c_str(); }
@@ -837,6 +898,7 @@ int fb_create(int device, fb_ctx** out) {
             cudaStreamCreateWithFlags(&c->s_alt, cudaStreamNonBlocking) == cudaSuccess;
   for (cudaEvent_t* e : {&c->ev_start, &c->ev_kstart, &c->ev_kend, &c->ev_end})
     ok = ok && cudaEventCreate(e) == cudaSuccess;
+  ok = ok && cudaEventCreateWithFlags(&c->ev_upstream, cudaEventDisableTiming) == cudaSuccess;
   c->stream = c->own_stream;
   if (!ok || ensure_flags(c, 64) != FB_OK) {
     fb_destroy(c);
@@ -864,7 +926,7 @@ int fb_destroy(fb_ctx* c) {
   if (c->scratch) cudaFree(c->scratch);
   for (void* p : {(void*)c->flags_host, (void*)c->tab_host, (void*)c->tabd_host, (void*)c->scratch_host})
     if (p) cudaFreeHost(p);
-  for (cudaEvent_t e : {c->ev_start, c->ev_kstart, c->ev_kend, c->ev_end})
+  for (cudaEvent_t e : {c->ev_start, c->ev_kstart, c->ev_kend, c->ev_end, c->ev_upstream})
     if (e) cudaEventDestroy(e);
   for (auto& e : c->kev) cudaEventDestroy(e);
   for (auto& e : c->pev) cudaEventDestroy(e);
@@ -876,7 +938,16 @@ int fb_destroy(fb_ctx* c) {
 
 int fb_set_stream(fb_ctx* c, void* s) {
   if (!c) return fail(FB_ERR_PARAM, "null context");
-  c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+  const cudaStream_t cs = static_cast<cudaStream_t>(s);
+  if (cs == cudaStreamLegacy || cs == cudaStreamPerThread) {
+    // a default stream (torch's current stream is the legacy one, handle 0, bound as
+    // cudaStreamLegacy by the Python layer): run on own_stream, ordered after it at every call
+    c->stream = c->own_stream;
+    c->upstream = cs;
+  } else {
+    c->stream = cs ? cs : c->own_stream;
+    c->upstream = nullptr;
+  }
   return FB_OK;
 }
 
@@ -910,7 +981,7 @@ static int check_window(const fb_spatial* sp, long long rows, long long cols) {
 
 static int gpa_common(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int64_t halo_top,
                       int64_t halo_bottom, const fb_spatial* sp, double sigma_r, int32_t order, double center,
-                      double half_range, int32_t precision, fb_stats* stats) {
+                      double half_range, int32_t precision, fb_stats* stats, const Geom& geo = Geom()) {
   if (!ctx) return fail(FB_ERR_PARAM, "null context");
   if (count < 1 || !ins || !outs) return fail(FB_ERR_PARAM, "need at least one image");
   int rc = check_filter_args(sp, precision);
@@ -923,12 +994,13 @@ static int gpa_common(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int coun
     if (rc) return rc;
     rc = check_image(outs + i, "output", true);  // u8: quantised raster (save_pgm, image.py:96-99)
     if (rc) return rc;
-    if (halo_top < 0 || halo_bottom < 0 || halo_top + halo_bottom >= ins[i].rows)
+    if (!geo.separate() && (halo_top < 0 || halo_bottom < 0 || halo_top + halo_bottom >= ins[i].rows))
       return fail(FB_ERR_PARAM, "bad halo rows");
     if (ins[i].cols != ins[0].cols) return fail(FB_ERR_PARAM, "images of a batch must share their width");
-    const long long rows_out = ins[i].rows - halo_top - halo_bottom;
+    const long long rows_out = geo.separate() ? ins[i].rows : ins[i].rows - halo_top - halo_bottom;
     if (outs[i].rows != rows_out || outs[i].cols != ins[i].cols) return fail(FB_ERR_PARAM, "output shape mismatch");
-    rc = check_window(sp, rows_out, ins[i].cols);
+    // the reference checks the window against the whole image (conv.py:19-27)
+    rc = check_window(sp, geo.image_rows > 0 ? geo.image_rows : rows_out, ins[i].cols);
     if (rc) return rc;
   }
   Job j;
@@ -943,7 +1015,7 @@ static int gpa_common(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int coun
   j.tc = center;
   j.lo = center - half_range;
   j.hi = center + half_range;
-  return execute(ctx, ins, outs, count, (int)halo_top, (int)halo_bottom, j, precision, stats);
+  return execute(ctx, ins, outs, count, (int)halo_top, (int)halo_bottom, j, precision, stats, geo);
 }
 
 int fb_gpa_filter(fb_ctx* ctx, const fb_image* in, int64_t halo_top, int64_t halo_bottom, fb_image* out,
@@ -951,6 +1023,49 @@ int fb_gpa_filter(fb_ctx* ctx, const fb_image* in, int64_t halo_top, int64_t hal
                   int32_t precision, fb_stats* stats) {
   return gpa_common(ctx, in, out, 1, halo_top, halo_bottom, sp, sigma_r, order, center, half_range, precision,
                     stats);
+}
+
+int fb_gpa_filter_band(fb_ctx* ctx, const fb_image* in, const fb_image* above, const fb_image* below,
+                       int64_t row_origin, int64_t image_rows, fb_image* out, const fb_spatial* sp, double sigma_r,
+                       int32_t order, double center, double half_range, int32_t precision, fb_stats* stats) {
+  if (!ctx) return fail(FB_ERR_PARAM, "null context");
+  int rc = check_image(in, "input", true);
+  if (rc) return rc;
+  if (row_origin < 0 || image_rows < row_origin + in->rows || image_rows > (1ll << 30))
+    return fail(FB_ERR_PARAM, "band rows outside the image");
+  const long long above_rows = above ? above->rows : 0, below_rows = below ? below->rows : 0;
+  if (above_rows > row_origin || below_rows > image_rows - row_origin - in->rows)
+    return fail(FB_ERR_PARAM, "halo rows outside the image");
+  const size_t es = dtype_size(in->dtype);
+  bool contiguous = true;  // halos that are simply the rows next to `in` in the same buffer
+  for (const fb_image* h : {above, below}) {
+    if (!h) continue;
+    rc = check_image(h, "halo", true);
+    if (rc) return rc;
+    if (h->cols != in->cols || h->dtype != in->dtype) return fail(FB_ERR_PARAM, "halo rows must match the band");
+    const char* want = h == above ? static_cast<const char*>(in->data) - (size_t)h->rows * h->ld * es
+                                  : static_cast<const char*>(in->data) + (size_t)in->rows * in->ld * es;
+    contiguous = contiguous && h->ld == in->ld && h->on_device == in->on_device && h->data == want;
+  }
+  Geom geo;
+  geo.row_origin = row_origin;
+  geo.image_rows = image_rows;
+  if (contiguous) {
+    // one buffer [above | in | below]: the fb_gpa_filter path (host buffers pipelined in chunks)
+    fb_image whole = *in;
+    whole.data = above ? above->data : in->data;
+    whole.rows = above_rows + in->rows + below_rows;
+    geo.report_rows = above_rows;
+    return gpa_common(ctx, &whole, out, 1, above_rows, below_rows, sp, sigma_r, order, center, half_range,
+                      precision, stats, geo);
+  }
+  for (const fb_image* h : {above, below})
+    if (h && (!h->on_device || !in->on_device))
+      return fail(FB_ERR_PARAM, "halo rows in separate buffers need device-resident input and halos");
+  geo.above = above;
+  geo.below = below;
+  return gpa_common(ctx, in, out, 1, above_rows, below_rows, sp, sigma_r, order, center, half_range, precision,
+                    stats, geo);
 }
 
 int fb_gpa_filter_batch(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int32_t count, const fb_spatial* sp,
@@ -1012,6 +1127,7 @@ int fb_bilateral_exact(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_
     return fail(FB_ERR_WINDOW, "window half-width " + std::to_string(sp->half_width) + " too large for " +
                                    std::to_string(in->rows) + "x" + std::to_string(in->cols) + " image");
   FB_CUDA(cudaSetDevice(ctx->device));
+  if (int orc = order_after_caller(ctx)) return orc;
   const int W = sp->half_width, n = 2 * W + 1;
   std::vector<double> w(n);
   for (int k = 0; k < n; ++k) w[k] = sp->kind == FB_BOX ? 1.0 / n : sp->weights_1d[k];
@@ -1028,7 +1144,7 @@ int fb_bilateral_exact(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_
   FB_CUDA(cudaMallocAsync(&dw, n * sizeof(double), ctx->stream));
   FB_CUDA(cudaMemcpyAsync(dw, w.data(), n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
   if (!in->on_device) {
-    rc = grow(&ctx->in_stage[0], &ctx->in_stage_bytes[0], (size_t)in->rows * in->cols * ies);
+    rc = grow(ctx, &ctx->in_stage[0], &ctx->in_stage_bytes[0], (size_t)in->rows * in->cols * ies);
     if (rc) return rc;
     FB_CUDA(cudaMemcpy2DAsync(ctx->in_stage[0], in->cols * ies, in->data, in->ld * ies, in->cols * ies, in->rows,
                               cudaMemcpyHostToDevice, ctx->stream));
@@ -1036,7 +1152,7 @@ int fb_bilateral_exact(fb_ctx* ctx, const fb_image* in, fb_image* out, const fb_
     dld = in->cols;
   }
   if (!out->on_device) {
-    rc = grow(&ctx->out_stage[0], &ctx->out_stage_bytes[0], (size_t)out->rows * out->cols * 8);
+    rc = grow(ctx, &ctx->out_stage[0], &ctx->out_stage_bytes[0], (size_t)out->rows * out->cols * 8);
     if (rc) return rc;
     dout = ctx->out_stage[0];
     old = out->cols;
@@ -1092,7 +1208,7 @@ static int stage_input(fb_ctx* c, const fb_image* im, int slot, const void** d, 
     return FB_OK;
   }
   const size_t es = dtype_size(im->dtype);
-  int rc = grow(&c->in_stage[slot], &c->in_stage_bytes[slot], (size_t)im->rows * im->cols * es);
+  int rc = grow(c, &c->in_stage[slot], &c->in_stage_bytes[slot], (size_t)im->rows * im->cols * es);
   if (rc) return rc;
   FB_CUDA(cudaMemcpy2DAsync(c->in_stage[slot], im->cols * es, im->data, im->ld * es, im->cols * es, im->rows,
                             cudaMemcpyHostToDevice, c->stream));
@@ -1107,6 +1223,7 @@ int fb_kernel_error_sup(fb_ctx* ctx, int32_t order, double sigma_r, double half_
   if (!(sigma_r > 0 && half_range > 0)) return fail(FB_ERR_PARAM, "sigma_r and T must be positive");
   if (!(half_range < 1e6)) return fail(FB_ERR_PARAM, "T too large for the grid search");
   FB_CUDA(cudaSetDevice(ctx->device));
+  if (int orc = order_after_caller(ctx)) return orc;
   int rc = ensure_scratch(ctx, 64);
   if (rc) return rc;
   unsigned long long* bits = reinterpret_cast<unsigned long long*>(ctx->scratch);
@@ -1132,6 +1249,7 @@ int fb_error_stats(fb_ctx* ctx, const fb_image* a, const fb_image* b, double* li
                                   std::to_string(a->cols) + ") vs (" + std::to_string(b->rows) + ", " +
                                   std::to_string(b->cols) + ")");
   FB_CUDA(cudaSetDevice(ctx->device));
+  if (int orc = order_after_caller(ctx)) return orc;
   const int nb = error_stats_blocks(ctx->sm_count);
   rc = ensure_scratch(ctx, 2 * (size_t)nb + 4);
   if (rc) return rc;
@@ -1202,6 +1320,7 @@ int fb_convolve_direct(fb_ctx* ctx, const fb_image* in, fb_image* out, int32_t h
   rc = check_window(&sp, in->rows, in->cols);
   if (rc) return rc;
   FB_CUDA(cudaSetDevice(ctx->device));
+  if (int orc = order_after_caller(ctx)) return orc;
   const int n = 2 * half_width + 1;
   rc = ensure_flags(ctx, 1);
   if (rc) return rc;
@@ -1224,7 +1343,7 @@ int fb_convolve_direct(fb_ctx* ctx, const fb_image* in, fb_image* out, int32_t h
   void* dout = out->data;
   long long old = out->ld;
   if (!out->on_device) {
-    rc = grow(&ctx->out_stage[0], &ctx->out_stage_bytes[0], (size_t)out->rows * out->cols * 8);
+    rc = grow(ctx, &ctx->out_stage[0], &ctx->out_stage_bytes[0], (size_t)out->rows * out->cols * 8);
     if (rc) return rc;
     dout = ctx->out_stage[0];
     old = out->cols;

@@ -37,6 +37,18 @@ struct GpaArgs {
   int rows_in;        // rows in the buffer (incl. halos)
   int cols;
   int halo_top;       // buffer row of output row 0
+  int main_end;       // buffer row after the last output row (= rows_in - halo_bottom)
+  // Halo rows may live in other allocations (a neighbour rank's band, mapped over CUDA IPC):
+  // buffer row b < halo_top starts at element top_off + b * top_ld of f, row b >= main_end at
+  // bot_off + (b - main_end) * bot_ld (offsets in samples, relative to f).  A contiguous buffer
+  // has top_off = 0, top_ld = bot_ld = f_ld, bot_off = main_end * f_ld.  See sample_row().
+  long long top_off, top_ld, bot_off, bot_ld;
+  // Global geometry: output row 0 of the buffer is image row row_origin of an image_rows-row
+  // image.  Box kernels anchor their running sums (walks / tile segments) to image rows, so a
+  // pixel's value does not depend on how the image is split into bands, chunks or ranks.
+  long long row_origin;
+  int image_rows;
+  int lead;           // rows the first box walk / tile of the band starts above the band (anchoring)
   // current row band
   int band_row0;      // first output row of the band
   int band_rows;      // output rows in the band
@@ -77,8 +89,33 @@ struct GpaArgs {
   // (q_n, q_n) pairs for n < kWalkMaxCh: the box walker's two-step multipliers (walk_q)
   alignas(8) float rsc2[2 * 64];
   int walk_rows;      // output rows per thread of the box walker
-  int n_delta1;       // order Algorithm 1 picks for delta = 1 gray level (Horner-precision policy)
 };
+
+// Rows per box walk (kernel 1, both precisions): long walks amortise the 2W warm-up rows; shorter
+// ones (down to 64) while the grid would not give every SM several CTAs.  It depends on the image
+// (width, height) only, never on the band, and every length divides 256: a band starting at a
+// multiple of 256 image rows walks no rows above itself.
+inline int walk_rows(int wpad, int image_rows, int threads) {
+  const long long gx = (wpad + threads - 1) / threads;
+  int ch = 256;
+  while (ch > 64 && gx * ((image_rows + ch - 1) / ch) < 8 * 148) ch /= 2;
+  return ch;
+}
+// Rows between the start of the box walk / tile segment of length `seg` containing the band's
+// first row and that row (segments start at image rows that are multiples of seg).
+template <typename T>
+inline int box_lead(const GpaArgs<T>& a, int seg) {
+  return (int)((a.row_origin + a.band_row0) % seg);
+}
+
+// Sample offset (relative to f) of the start of buffer row b, clamped to the buffer (the
+// reference's edge replication, conv.py:51/62); the halo rows may come from separate buffers.
+template <typename T>
+__device__ __forceinline__ long long sample_row(const GpaArgs<T>& a, long long b) {
+  b = b < 0 ? 0 : (b >= a.rows_in ? a.rows_in - 1 : b);
+  return b < a.halo_top ? a.top_off + b * a.top_ld
+                        : (b < a.main_end ? b * a.f_ld : a.bot_off + (b - a.main_end) * a.bot_ld);
+}
 
 constexpr int kWalkMaxCh = 64;              // channels (N+1) the register-resident box walker holds
 

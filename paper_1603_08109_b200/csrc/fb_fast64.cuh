@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(KD_THREADS) k1d_box_walk(const __grid_constant
   const int N = a.N;
   const int CH = a.walk_rows;
   const int pc = blockIdx.x * KD_THREADS + threadIdx.x;
-  const int r0 = blockIdx.y * CH;
+  const int r0 = blockIdx.y * CH - a.lead;  // walks start at image rows = multiples of CH (fb_fast.cuh)
   const int rows_here = min(CH, a.band_rows - r0);
   const int scol = min(max(pc - W, 0), a.cols - 1);
   const bool own_col = pc >= W && pc < W + a.cols;
@@ -58,18 +58,19 @@ __global__ void __launch_bounds__(KD_THREADS) k1d_box_walk(const __grid_constant
   unsigned long long bad_nf = ~0ull, bad_rg = ~0ull;
   double* vp = a.v + pc;
   // samples two steps ahead in registers (loads of step st+2 overlap steps st, st+1)
-  double ve0 = load_sample(a.f, a.f_dtype, clamp_row(r0 - W) * a.f_ld + scol);
-  double vl0 = load_sample(a.f, a.f_dtype, clamp_row(r0 - 3 * W - 1) * a.f_ld + scol);
-  double ve1 = load_sample(a.f, a.f_dtype, clamp_row(r0 - W + 1) * a.f_ld + scol);
-  double vl1 = load_sample(a.f, a.f_dtype, clamp_row(r0 - 3 * W) * a.f_ld + scol);
+  auto sample = [&](int band_row) { return load_sample(a.f, a.f_dtype, sample_row(a, row_base + band_row) + scol); };
+  double ve0 = sample(r0 - W);
+  double vl0 = sample(r0 - 3 * W - 1);
+  double ve1 = sample(r0 - W + 1);
+  double vl1 = sample(r0 - 3 * W);
   for (int st = 0; st < steps; ++st) {
     const int enter = r0 - W + st;
     const double fe = ve0, fl = vl0;
     ve0 = ve1;
     vl0 = vl1;
-    ve1 = load_sample(a.f, a.f_dtype, clamp_row(enter + 2) * a.f_ld + scol);
-    vl1 = load_sample(a.f, a.f_dtype, clamp_row(enter + 1 - 2 * W) * a.f_ld + scol);
-    if (a.check && own_col && enter >= r0 && enter < r0 + rows_here) {
+    ve1 = sample(enter + 2);
+    vl1 = sample(enter + 1 - 2 * W);
+    if (a.check && own_col && enter >= r0 && enter >= 0 && enter < r0 + rows_here) {
       const unsigned long long idx = (unsigned long long)clamp_row(enter) * a.cols + scol;
       if (!isfinite(fe) && bad_nf == ~0ull) bad_nf = idx;
       if ((fe < a.lo || fe > a.hi) && bad_rg == ~0ull) bad_rg = idx;
@@ -87,7 +88,7 @@ __global__ void __launch_bounds__(KD_THREADS) k1d_box_walk(const __grid_constant
       S[n] += ce - cl;
     }
     const int out_row = enter - W;
-    if (col_ok && out_row >= r0) {
+    if (col_ok && out_row >= r0 && out_row >= 0) {
       double* dst = vp + (long long)out_row * a.rstride;
 #pragma unroll
       for (int n = 0; n < NCH; ++n, dst += a.pitch)
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(KT_THREADS) k1d_gen_vpass(const __grid_constan
   const int tc = threadIdx.x % KT_TC;
   const int g = threadIdx.x / KT_TC;
   const int pc = blockIdx.x * KT_TC + tc;
-  const int o0 = blockIdx.y * KT_RB;
+  const int o0 = blockIdx.y * KT_RB - (KIND == kKindBox ? a.lead : 0);  // box: anchored to image rows
   const int scol = min(max(pc - W, 0), a.cols - 1);
 
   double cst[NS], xst[NS];
@@ -135,7 +136,7 @@ __global__ void __launch_bounds__(KT_THREADS) k1d_gen_vpass(const __grid_constan
     }
 #pragma unroll
     for (int t = 0; t < NS; ++t)
-      fv[t] = g + KT_RG * t < TR ? load_sample(a.f, a.f_dtype, brows[t] * a.f_ld + scol) : 0.0;
+      fv[t] = g + KT_RG * t < TR ? load_sample(a.f, a.f_dtype, sample_row(a, brows[t]) + scol) : 0.0;
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
       const int i = g + KT_RG * t;
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(KT_THREADS) k1d_gen_vpass(const __grid_constan
       if (i < TR) {
         if (a.check) {
           const int o = o0 + i - W;
-          const bool own = i >= W && i < W + KT_RB && o < a.band_rows && pc >= W && pc < W + a.cols;
+          const bool own = i >= W && i < W + KT_RB && o >= 0 && o < a.band_rows && pc >= W && pc < W + a.cols;
           const unsigned long long idx = (unsigned long long)brows[t] * a.cols + scol;
           if (own && !isfinite(fv[t]) && bad_nf == ~0ull) bad_nf = idx;
           if (own && (fv[t] < a.lo || fv[t] > a.hi) && bad_rg == ~0ull) bad_rg = idx;
@@ -208,7 +209,7 @@ __global__ void __launch_bounds__(KT_THREADS) k1d_gen_vpass(const __grid_constan
     if (col_ok) {
 #pragma unroll
       for (int r = 0; r < KT_R; ++r)
-        if (o0 + ob + r < a.band_rows) vp[(long long)r * a.rstride] = acc[r];
+        if (o0 + ob + r < a.band_rows && o0 + ob + r >= 0) vp[(long long)r * a.rstride] = acc[r];
     }
   }
 }
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(KD2_THREADS, kd2_ctas<KIND>())
   // warp-level release after the pass
   // (the proxy fence of fb_fast.cuh's kernel 2: stage reads ordered before the refill TMA)
   auto release = [&](int it) {
-    if constexpr (FB_K2_PROXY_FENCE) fast::fence_proxy_async_smem();
+    fast::fence_proxy_async_smem();
     if constexpr (KIND == kKindBox) {
       fast::mbar_arrive(empty + it % STAGES);
     } else {
@@ -467,19 +468,20 @@ int launch_pair64(cudaStream_t st, GpaArgs<double>& a, const KernelEvents& ev) {
   a.tabd = a.tabd_seq;  // both kernel 1 variants use the sequential recurrence
   void (*k1)(const GpaArgs<double>) = k1d_gen_vpass<KIND, WT>;
   size_t s1 = kt_smem_bytes(W);
-  dim3 g1((a.wpad + KT_TC - 1) / KT_TC, (a.band_rows + KT_RB - 1) / KT_RB), b1(KT_THREADS);
+  a.lead = KIND == kKindBox ? box_lead(a, KT_RB) : 0;
+  dim3 g1((a.wpad + KT_TC - 1) / KT_TC, (a.band_rows + a.lead + KT_RB - 1) / KT_RB), b1(KT_THREADS);
   if constexpr (KIND == kKindBox) {
-    if (a.N + 1 <= kWalkMaxCh && (long long)a.wpad * a.band_rows >= (4ll << 20)) {
+    if (a.N + 1 <= kWalkMaxCh && (long long)a.wpad * a.image_rows >= (4ll << 20)) {
       static void (*const walkers[8])(const GpaArgs<double>) = {
           k1d_box_walk<8>, k1d_box_walk<16>, k1d_box_walk<24>, k1d_box_walk<32>,
           k1d_box_walk<40>, k1d_box_walk<48>, k1d_box_walk<56>, k1d_box_walk<64>};
       k1 = walkers[(a.N + 1 + 7) / 8 - 1];
       s1 = 0;
       const int gx = (a.wpad + KD_THREADS - 1) / KD_THREADS;
-      int ch = 256;
-      while (ch > 8 && ch > 2 * W && (long long)gx * ((a.band_rows + ch - 1) / ch) < 8 * 148) ch /= 2;
+      const int ch = walk_rows(a.wpad, a.image_rows, KD_THREADS);
       a.walk_rows = ch;
-      g1 = dim3(gx, (a.band_rows + ch - 1) / ch);
+      a.lead = box_lead(a, ch);
+      g1 = dim3(gx, (a.band_rows + a.lead + ch - 1) / ch);
       b1 = dim3(KD_THREADS);
     }
   }

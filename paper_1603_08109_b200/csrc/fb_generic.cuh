@@ -50,16 +50,16 @@ __global__ void __launch_bounds__(K1_TC * K1_RG) k1_gen_vpass(const GpaArgs<T> a
   const int tc = threadIdx.x % K1_TC;
   const int g = threadIdx.x / K1_TC;
   const int pc = blockIdx.x * K1_TC + tc;
-  const int o0 = blockIdx.y * K1_RB;
+  const int o0 = blockIdx.y * K1_RB - (KIND == kKindBox ? a.lead : 0);  // box: anchored to image rows
   const int scol = min(max(pc - W, 0), a.cols - 1);
 
   for (int i = g; i < TR; i += K1_RG) {
     const int o = o0 + i - W;
     long long brow = (long long)a.halo_top + a.band_row0 + o;
     brow = brow < 0 ? 0 : (brow >= a.rows_in ? a.rows_in - 1 : brow);
-    const double fv = load_sample(a.f, a.f_dtype, brow * a.f_ld + scol);
+    const double fv = load_sample(a.f, a.f_dtype, sample_row(a, brow) + scol);
     if (a.check) {
-      const bool own = i >= W && i < W + K1_RB && o < a.band_rows && pc >= W && pc < W + a.cols;
+      const bool own = i >= W && i < W + K1_RB && o >= 0 && o < a.band_rows && pc >= W && pc < W + a.cols;
       check_sample(a.flags, own, fv, a.lo, a.hi, (unsigned long long)brow * a.cols + scol);
     }
     T x, e;
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(K1_TC * K1_RG) k1_gen_vpass(const GpaArgs<T> a
       for (int k = 0; k <= 2 * W; ++k) s += cs[(ob + k) * K1_TC + tc];
       for (int r = 0; r < K1_R; ++r) {
         const int o = o0 + ob + r;
-        if (col_ok && o < a.band_rows) vp[(long long)o * a.rstride + pc] = s;
+        if (col_ok && o >= 0 && o < a.band_rows) vp[(long long)o * a.rstride + pc] = s;
         s += cs[(ob + r + 2 * W + 1) * K1_TC + tc] - cs[(ob + r) * K1_TC + tc];
       }
     } else {

@@ -181,9 +181,10 @@ def test_batch_matches_single_and_names_bad_image():
 
 
 def test_chunked_host_pipeline_matches_device_path():
-    """Host images > 4 MP are pipelined in 8 row chunks over three streams.  The box walker's
-    running sums restart at chunk boundaries, so both partitions are compared with the fp64 path
-    (itself pinned to the reference at 1e-9) rather than with each other bitwise."""
+    """Host images > 4 MP are pipelined in row chunks (multiples of 256 rows) over three streams.
+    The box walks start at image rows that are multiples of 256 whatever the chunking, so the
+    chunked host path is bit-identical to one device-resident call; both are also checked against
+    the fp64 path (itself pinned to the reference at 1e-9)."""
     torch = pytest.importorskip("torch")
     cfg = synth.CONFIGS["c4"]
     img = synth.config_image(cfg, height=2304, width=2048)
@@ -193,7 +194,7 @@ def test_chunked_host_pipeline_matches_device_path():
         assert stats["h2d_bytes"] == img.nbytes and stats["d2h_bytes"] == host.nbytes
         dev = gpa_filter(torch.from_numpy(img).cuda(), k, 25.0, N, precision="f32").cpu().numpy()
         ref = gpa_filter(img, k, 25.0, N, precision="f64")
-        assert np.max(np.abs(host - ref)) <= 5e-4
+        assert np.array_equal(host, dev)
         assert np.max(np.abs(dev - ref)) <= 5e-4
 
 
@@ -339,3 +340,41 @@ def test_full_size_c4_windows():
     windows = [(0, 0, 48, 48), (H - 48, Wd - 48, 48, 48), (H // 2 + 5, Wd // 3 + 7, 64, 64),
                (8191, 8100, 40, 40), (H - 30, 0, 30, 64)]
     _window_check(img, out.astype(np.float64), k, cfg.sigma_r, N, windows, F32_TOL)
+
+
+def test_default_stream_work_is_ordered_before_the_call():
+    """A tensor still being written by torch on the legacy default stream is read only after that
+    write (fb_set_stream(cudaStreamLegacy): the context's stream waits for it at every call)."""
+    torch = pytest.importorskip("torch")
+    x = torch.zeros((1024, 1024), dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    k = make_spatial_kernel("box", half_width=5)
+    for _ in range(3):
+        torch.cuda._sleep(100_000_000)  # ~50 ms spin on the default stream, then the write
+        x.fill_(200.0)
+        out = gpa_filter(x, k, 50.0, 10, precision="f32").cpu().numpy()
+        assert np.max(np.abs(out - 200.0)) <= 1e-4
+        x.zero_()
+
+
+def test_concurrent_calls_from_threads():
+    """ctypes releases the GIL: calls from several host threads share one device context, which
+    the binding serialises (a context is not re-entrant)."""
+    import threading
+    rng = np.random.default_rng(7)
+    imgs = [np.floor(rng.uniform(0, 256, (300 + 17 * i, 257))).astype(np.float32) for i in range(6)]
+    k = make_spatial_kernel("gaussian", sigma_s=3.0)
+    want = [gpa_filter(im, k, 40.0, 15, precision="f32") for im in imgs]
+    got = [None] * len(imgs)
+
+    def work(i):
+        for _ in range(5):
+            got[i] = gpa_filter(imgs[i], k, 40.0, 15, precision="f32")
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(len(imgs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for w, g in zip(want, got):
+        assert np.array_equal(w, g)

@@ -2,7 +2,7 @@
 kernel 2 = the fast horizontal pass + fp64 Horner; and the fp64 walker / kernel 2 of
 fb_fast64.cuh) and of kernel 2's epilogue paths.
 
-The walker runs when (cols + 2W) x band_rows >= 4 Mi samples and N+1 <= 64, so these images are
+The walker runs when (cols + 2W) x image rows >= 4 Mi samples and N+1 <= 64, so these images are
 ~2100^2.  Full images are compared with the fp64 path (pinned to the reference at 1e-9 by
 test_gpu_parity.py); windows are compared with the oracle itself.
 """
@@ -62,8 +62,8 @@ def test_walker_matches_oracle_and_fp64(W, N, sigma_r, dtype):
 
 
 def test_fp64_walker_bands_and_halos_are_exact():
-    """The fp64 walker (fb_fast64.cuh) is partition-independent to fp64 rounding: two bands and a
-    halo-band call reproduce the single call to 1e-10."""
+    """The fp64 walker (fb_fast64.cuh) is partition-independent: two bands and a band call with
+    separate halo buffers reproduce the single call bit for bit."""
     torch = pytest.importorskip("torch")
     img = synth.config_image("c4", height=4096, width=2048)
     k = make_spatial_kernel("box", half_width=20)
@@ -78,16 +78,19 @@ def test_fp64_walker_bands_and_halos_are_exact():
     finally:
         _native.set_workspace_limit(8 << 30)
     assert st["bands"] == 2
-    assert np.max(np.abs(banded - full)) <= 1e-10
-    r0, r1 = 1000, 3100
-    ext = torch.from_numpy(np.ascontiguousarray(img[r0 - W:r1 + W])).cuda()
+    assert np.array_equal(banded, full)
+    r0, r1 = 1024, 3100
+    band = torch.from_numpy(np.ascontiguousarray(img[r0:r1])).cuda()
+    above = torch.from_numpy(np.ascontiguousarray(img[r0 - W:r0])).cuda()
+    below = torch.from_numpy(np.ascontiguousarray(img[r1:r1 + W])).cuda()
     out = torch.empty((r1 - r0, img.shape[1]), dtype=torch.float64, device="cuda")
-    _native.gpa(ext, out, k, 25.0, N, 128.0, 128.0, _native.FB_PREC_F64, 0, halo_top=W, halo_bottom=W)
-    assert np.max(np.abs(out.cpu().numpy() - full[r0:r1])) <= 1e-10
+    _native.gpa_band(band, out, k, 25.0, N, 128.0, 128.0, _native.FB_PREC_F64, r0, 4096, above, below, 0)
+    assert np.array_equal(out.cpu().numpy(), full[r0:r1])
 
 
 def test_walker_band_partitions_agree():
-    """Several walker bands (workspace limit) and an explicit halo-band call agree with one band."""
+    """Several walker bands (workspace limit) and band calls with separate halo buffers are
+    bit-identical to one band (results independent of the parallel decomposition)."""
     torch = pytest.importorskip("torch")
     img = synth.config_image("c4", height=4096, width=2048)
     k = make_spatial_kernel("box", half_width=20)
@@ -104,9 +107,20 @@ def test_walker_band_partitions_agree():
     assert one["bands"] == 1 and many["bands"] == 2
     ref64 = gpa_filter(img, k, 25.0, N, precision="f64")
     assert np.max(np.abs(full - ref64)) <= 5e-4
-    assert np.max(np.abs(banded - ref64)) <= 5e-4
-    # rows [1000, 3100) from a buffer holding only those rows plus W halo rows each side
-    r0, r1, W = 1000, 3100, 20
+    assert np.array_equal(banded, full)  # walks start at image rows = multiples of 256 in both
+    H, W = img.shape[0], 20
+    # rows [1024, 3100) from buffers holding only those rows, and W halo rows each side in separate
+    # buffers (a rank's band and its neighbours' rows, fb_gpa_filter_band): the same bits
+    for r0, r1, top in ((1024, 3100, W), (0, 1280, 0), (2816, H, W), (1000, 3100, W + 1000 % 256)):
+        band = torch.from_numpy(np.ascontiguousarray(img[r0:r1])).cuda()
+        above = torch.from_numpy(np.ascontiguousarray(img[r0 - top:r0])).cuda() if top else None
+        below = torch.from_numpy(np.ascontiguousarray(img[r1:r1 + W])).cuda() if r1 < H else None
+        out = torch.empty((r1 - r0, img.shape[1]), dtype=torch.float64, device="cuda")
+        _native.gpa_band(band, out, k, 25.0, N, 128.0, 128.0, _native.FB_PREC_F32, r0, H, above, below, 0)
+        assert np.array_equal(out.cpu().numpy(), full[r0:r1]), (r0, r1)
+    # a band off the 256-row grid with only W halo rows: its first walk re-reads rows it does not
+    # have (replicated), so the bits differ -- still the same filter to fp32 rounding
+    r0, r1 = 1000, 3100
     ext = torch.from_numpy(np.ascontiguousarray(img[r0 - W:r1 + W])).cuda()
     out = torch.empty((r1 - r0, img.shape[1]), dtype=torch.float32, device="cuda")
     _native.gpa(ext, out, k, 25.0, N, 128.0, 128.0, _native.FB_PREC_F32, 0, halo_top=W, halo_bottom=W)
@@ -114,20 +128,21 @@ def test_walker_band_partitions_agree():
 
 
 def test_host_band_with_halos_chunked():
-    """The multi-GPU e2e leg: a host-resident band plus halo rows, pipelined in row chunks through
-    fb_gpa_filter (H2D / kernels / D2H on three streams), equals the same rows of the whole image."""
+    """The multi-GPU e2e leg: a host-resident band with its halo rows in the same buffer
+    (fb_gpa_filter_band with adjacent halos), pipelined in row chunks (H2D / kernels / D2H on three
+    streams), is bit-identical to the same rows of the whole image."""
     img = synth.config_image("c4", height=4096, width=2048)
     k = make_spatial_kernel("box", half_width=20)
     N, W = 57, 20
     full = gpa_filter(img, k, 25.0, N, precision="f32")
-    for r0, r1 in ((0, 2300), (1000, 3300), (1800, 4096)):
+    for r0, r1 in ((0, 2304), (1024, 3328), (1792, 4096)):
         top, bottom = min(W, r0), min(W, 4096 - r1)
         ext = np.ascontiguousarray(img[r0 - top:r1 + bottom])
         out = np.empty((r1 - r0, img.shape[1]), dtype=np.float64)
-        st = _native.gpa(ext, out, k, 25.0, N, 128.0, 128.0, _native.FB_PREC_F32, 0, halo_top=top,
-                         halo_bottom=bottom)
+        st = _native.gpa_band(ext[top:top + r1 - r0], out, k, 25.0, N, 128.0, 128.0, _native.FB_PREC_F32, r0,
+                              4096, ext[:top] if top else None, ext[top + r1 - r0:] if bottom else None, 0)
         assert st["h2d_bytes"] == ext.nbytes and st["d2h_bytes"] == out.nbytes
-        assert np.max(np.abs(out - full[r0:r1])) <= 5e-4, (r0, r1)  # walks restart at other rows
+        assert np.array_equal(out, full[r0:r1]), (r0, r1)
 
 
 @pytest.mark.parametrize("width", [128, 130, 131, 133, 1029])

@@ -51,3 +51,17 @@ def test_no_gpu_fails_loudly():
     from paper_1603_08109_b200 import NativeError, gpa_filter, make_spatial_kernel
     with pytest.raises(NativeError):
         gpa_filter(np.zeros((8, 8)), make_spatial_kernel("box", half_width=1), 30.0, 5)
+
+
+def test_stale_library_is_refused(monkeypatch):
+    """The in-tree library carries the hash of the sources it was built from (fb_build_id); a
+    library built from other sources must not load (a stale .so can never be the one that runs)."""
+    if not os.path.exists(_native.LIB_PATH):
+        pytest.skip("libfbgpu.so not built (run __graft_entry__.build())")
+    from paper_1603_08109_b200 import _buildid
+    lib = _native.load_library()
+    assert lib.fb_build_id().decode() == _buildid.source_build_id()
+    monkeypatch.setattr(_native, "_lib", None)
+    monkeypatch.setattr(_buildid, "source_build_id", lambda *a: "0123456789abcdef")
+    with pytest.raises(_native.NativeError, match="other sources"):
+        _native.load_library()
