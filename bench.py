@@ -4,7 +4,9 @@
 
 A "step" is one pass of the filter over the config's whole workload:
   c4 (default): one 16384^2 float32 image, box W=20, sigma_r=25, delta=1 -> N=57;
-                at N>1 GPUs: row bands + P2P halo exchange + gather to rank 0.
+                at N>1 GPUs: row bands (starts at multiples of 256 rows) whose kernel 1 reads
+                the neighbours' halo rows in place and whose kernel 2 writes into rank 0's
+                output (CUDA IPC; no collective).
   c3: 64 float32 images of 2048^2, Gaussian sigma_s=8, sigma_r=20, delta=1 -> N=76; by image.
   c0/c1/c2: single images (replicas at N>1).
 `value` = megapixels/s over all ranks with inputs resident in HBM (device
@@ -22,7 +24,6 @@ import argparse
 import json
 import math
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -63,59 +64,68 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 100 ms while the timed region runs."""
+    """SM clock + clock-event (throttle) reasons sampled every ~5 ms through NVML while the timed
+    region runs (a short timed region still gets samples; nvidia-smi -lms takes ~0.3 s to start).
+    The timed region starts only after the first sample has been taken."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    def __init__(self, cuda_index: int):
+        self.cuda_index = cuda_index
+        self.samples = []  # (sm_mhz, reasons bitmask)
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self.error = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda._get_nvml_device_index(self.cuda_index))
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.thread = threading.Thread(target=self._run, daemon=True)
             self.thread.start()
-            time.sleep(0.15)
-        except Exception:
-            self.proc = None
+            t0 = time.monotonic()
+            while not self.samples and time.monotonic() - t0 < 1.0:
+                time.sleep(0.001)
+        except Exception as e:  # no NVML: the line says so (samples = 0)
+            self.error = repr(e)
+            self.h = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)),
+                                     int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+            except Exception as e:
+                self.error = repr(e)
+                return
+            time.sleep(0.005)
 
     def __exit__(self, *exc):
-        if self.proc is not None:
-            time.sleep(0.15)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.h is not None:
+            self.thread.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = max(mx, float(parts[1]))
-            except ValueError:
-                continue
-            for name, val in zip(names, parts[2:6]):
-                if val.lower() == "active":
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0, "error": self.error}
+        reasons = set()
+        for _, bits in self.samples:
+            for name, const in self.REASONS:
+                if bits & getattr(self.nv, const, 0):
                     reasons.add(name)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        sm = [m for m, _ in self.samples]
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(np.min(sm)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sm), "source": "NVML, 5 ms"}
 
 
 def algorithmic_bytes(cfg, N):
@@ -294,13 +304,19 @@ def main():
     dev_out = [torch.empty(im.shape, dtype=torch.float32, device=dev) for im in host_imgs]
     my_pixels = sum(im.shape[0] * im.shape[1] for im in host_imgs)
     root_full = None
-    peer = None
+    peer = pin = None
     if bands is not None:
-        # the final gather is fused into kernel 2: every rank writes its rows straight into the
-        # root's buffer over NVLink / NVSwitch (sharding.PeerOutput, CUDA IPC)
+        # no collective on the data path: kernel 1 reads the W halo rows in place from the
+        # neighbours' input bands (sharding.PeerInput, CUDA IPC over NVLink / NVSwitch), and the
+        # final gather is fused into kernel 2, which writes every rank's rows straight into the
+        # root's buffer (sharding.PeerOutput); the hand-offs are store flags
         if rank == 0:
             root_full = torch.empty((cfg.height, cfg.width), dtype=torch.float32, device=dev)
         peer = sharding.PeerOutput(root_full, (cfg.height, cfg.width), torch.float32, rank, local)
+        pin = sharding.PeerInput(dev_imgs[0], bands, rank, local)
+        torch.cuda.synchronize(dev)
+        pin.publish()  # the inputs are written once: one hand-off before the steps
+        pin.wait_neighbours()
     flush = None
     if cfg.pixels * 4 <= 126e6:
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -310,11 +326,10 @@ def main():
 
     def step(record=False):
         if bands is not None:
-            ext = sharding.exchange_halos(dev_imgs[0], W, rank, world, bands)
-            top, bottom = bands.halos(rank)
             r0, r1 = bands.bounds(rank)
-            st = _native.gpa(ext, peer.band(r0, r1), kernel, cfg.sigma_r, N, 128.0, 128.0, _native.FB_PREC_F32,
-                             local, halo_top=top, halo_bottom=bottom)
+            st = _native.gpa_band(dev_imgs[0], peer.band(r0, r1), kernel, cfg.sigma_r, N, 128.0, 128.0,
+                                  _native.FB_PREC_F32, row_origin=r0, image_rows=cfg.height, above=pin.above,
+                                  below=pin.below, device=local)
             sts = [st]
             peer.done()
         elif len(dev_imgs) > 1:
@@ -376,8 +391,12 @@ def main():
             else:
                 if host_ext is not None:
                     top, bottom = bands.halos(rank)
-                    _native.gpa(pinned_in[0], pinned_out[0], kernel, cfg.sigma_r, N, 128.0, 128.0,
-                                _native.FB_PREC_F32, local, halo_top=top, halo_bottom=bottom)
+                    r0, r1 = bands.bounds(rank)
+                    ext = pinned_in[0]
+                    _native.gpa_band(ext[top:top + r1 - r0], pinned_out[0], kernel, cfg.sigma_r, N, 128.0, 128.0,
+                                     _native.FB_PREC_F32, row_origin=r0, image_rows=cfg.height,
+                                     above=ext[:top] if top else None, below=ext[top + r1 - r0:] if bottom else None,
+                                     device=local)
                 else:
                     gpa_filter(pinned_in[0], kernel, cfg.sigma_r, N, precision="f32", device=local,
                                out=pinned_out[0])
@@ -408,12 +427,13 @@ def main():
                "path": ("gpa_filter_batch" if len(pinned_in) > 1 else "gpa_filter")
                + "(pinned float32 numpy in, out= pinned float64 numpy): H2D, kernels and D2H pipelined on "
                  "three streams inside the call"
-               + ("; at N>1 each rank filters its band from host memory through fb_gpa_filter with its "
+               + ("; at N>1 each rank filters its band from host memory through fb_gpa_filter_band with its "
                   "halo rows (libfbgpu C ABI), output rows to its own pinned buffer" if bands is not None else "")}
 
     if peer is not None:
-        dist.barrier()  # every rank is done writing into the root's buffer before unmapping
+        dist.barrier()  # teardown: every rank is done with the peer mappings before unmapping
         peer.close()
+        pin.close()
     if rank != 0:
         if world > 1:
             dist.barrier()

@@ -77,8 +77,26 @@ def load_library(path: str | None = None) -> ctypes.CDLL:
             raise NativeError(f"{path} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
         lib = ctypes.CDLL(path)
         missing = [n for n in EXPORTED_SYMBOLS if not hasattr(lib, n)]
-        if missing:
+        if missing and path == LIB_PATH:
             raise NativeError(f"{path} lacks {', '.join(missing)}: stale build, rerun __graft_entry__.build()")
+        if missing:  # an older A/B build: bind what it has
+            class _Lib:
+                def __init__(self, lib):
+                    self._lib = lib
+
+                def __getattr__(self, name):
+                    try:
+                        return getattr(self._lib, name)
+                    except AttributeError:
+                        return _Stub()
+
+            class _Stub:
+                argtypes = restype = None
+
+                def __call__(self, *a):
+                    raise NativeError("symbol missing from this A/B build")
+
+            lib = _Lib(lib)
         P = ctypes.POINTER
         vp = ctypes.c_void_p
         lib.fb_create.argtypes = [ctypes.c_int, P(vp)]

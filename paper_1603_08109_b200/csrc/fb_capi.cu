@@ -215,9 +215,8 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
   }
   // Box walker multipliers: it steps each channel parity by two orders at once,
   // c_n = c_{n-2} * x^2 * q_n with q_n = fl32(1/sqrt((n-1) n)) (q_1 = 1: c_1 = c_0 x), so the
-  // even and odd chains are independent.  Stored as (q_n, q_n) pairs for packed multiplies.
-  for (int m = 0; m < kWalkMaxCh; ++m)
-    a.rsc2[2 * m] = a.rsc2[2 * m + 1] = walk_q(m);
+  // even and odd chains are independent (read as (q_2k, q_2k+1) pairs for packed multiplies).
+  for (int m = 0; m < kWalkMaxCh; ++m) a.walkq[m] = walk_q(m);
   // channel constants 1/sqrt(m), sqrt(m) (rounded once from double), uploaded when N changes
   if (j.N + 1 > ctx->tab_cap) {
     ctx->realloc_seen = true;

@@ -86,8 +86,8 @@ struct GpaArgs {
   // Tap pairs for packed FFMA2 (fp32 fast path): wq[2a] = w[a], wq[2a+1] = w[a-1],
   // a = 0 .. 2W+1, with w[-1] = w[2W+1] = 0 (box: all ones).
   alignas(8) float wq[2 * (2 * kFastMaxW + 2)];
-  // (q_n, q_n) pairs for n < kWalkMaxCh: the box walker's two-step multipliers (walk_q)
-  alignas(8) float rsc2[2 * 64];
+  // the box walker's two-step multipliers q_n = walk_q(n), n < kWalkMaxCh (read as (q_2k, q_2k+1) pairs)
+  alignas(8) float walkq[64];
   int walk_rows;      // output rows per thread of the box walker
 };
 

@@ -49,7 +49,11 @@ if args.e2e:
     sys.exit(0)
 d = torch.from_numpy(img).cuda()
 out = torch.empty(img.shape, dtype=torch.float32, device="cuda")
+k1s, k2s = [], []
 for _ in range(args.reps):
     st = _native.gpa(d, out, k, cfg.sigma_r, N, 128.0, 128.0, _native.FB_PREC_F32, 0)
+    k1s.append(st["k1_ms"])
+    k2s.append(st["k2_ms"])
 torch.cuda.synchronize()
-print(f"{args.lib or ''} {args.config} {img.shape} N={N} k1_ms={st['k1_ms']:.3f} k2_ms={st['k2_ms']:.3f} bands={st['bands']}")
+print(f"{args.lib or ''} {args.config} {img.shape} N={N} k1_ms={st['k1_ms']:.3f} k2_ms={st['k2_ms']:.3f} "
+      f"median k1={np.median(k1s):.3f} k2={np.median(k2s):.3f} bands={st['bands']}")
