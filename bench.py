@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra-legs", action="store_true",
+                    help="skip the fp64 leg and the per-config device legs of the other configs")
     ap.add_argument("--cpu-sample-mp", type=float, default=0.0, help="override the CPU sample size (MP)")
     return ap.parse_args()
 
@@ -128,11 +130,12 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm), "source": "NVML, 5 ms"}
 
 
-def algorithmic_bytes(cfg, N):
-    """Per pixel: B_alg = 2 s_io + 2 (N+1) 4 and the split over the two kernels."""
+def algorithmic_bytes(cfg, N, ch_bytes=4):
+    """Per pixel: B_alg = 2 s_io + 2 (N+1) s_ch and the split over the two kernels
+    (s_ch = 4 for the fp32 planes, 8 for the fp64 path's planes)."""
     s_in = np.dtype(cfg.dtype).itemsize
     s_out = 4  # device-resident runs write float32
-    ch = (N + 1) * 4
+    ch = (N + 1) * ch_bytes
     return {"pipeline": s_in + s_out + 2 * ch, "k1": s_in + ch, "k2": ch + s_in + s_out}
 
 
@@ -260,6 +263,117 @@ def config_block(cfg, N, world):
 
 
 # ----------------------------------------------------------------------------- our arm (GPU)
+def _gen_image(args):
+    cfg_name, index = args
+    return synth.config_image(synth.CONFIGS[cfg_name], index)
+
+
+def config_images(cfg, indices):
+    """The seeded synthetic images `indices` of a config, generated on all host cores."""
+    indices = list(indices)
+    if len(indices) <= 2:
+        return [synth.config_image(cfg, i) for i in indices]
+    import multiprocessing as mp
+    with mp.get_context("fork").Pool(min(len(indices), os.cpu_count() or 1)) as pool:
+        return pool.map(_gen_image, [(cfg.name, i) for i in indices])
+
+
+def kernel_roofline(cfg, N, per_launch_ms, px_per_launch, launches, step_ms_total, ch_bytes=4):
+    """Per-kernel achieved HBM GB/s and FP32 TFLOP/s (algorithmic bytes / flops per launch over
+    the launch's CUDA-event time) and the dominant kernel's bound and fraction of peak."""
+    hbm_peak, _ = peaks()
+    bpp = algorithmic_bytes(cfg, N, ch_bytes)
+    fpp = algorithmic_flops(cfg, N)
+    kernels = {}
+    for name in ("k1", "k2"):
+        t = per_launch_ms[name] * 1e-3
+        kernels[name] = {
+            "avg_launch_ms": t * 1e3,
+            "share_of_step": per_launch_ms[name] * launches / max(1e-9, step_ms_total),
+            "hbm_gbs": bpp[name] * px_per_launch / t / 1e9,
+            "hbm_frac": bpp[name] * px_per_launch / t / 1e9 / hbm_peak,
+            "fp32_tflops": fpp[name] * px_per_launch / t / 1e12,
+            "fp32_frac": fpp[name] * px_per_launch / t / 1e12 / FP32_NOMINAL_TFLOPS,
+            "alg_bytes_per_px": bpp[name],
+        }
+    dom = max(("k1", "k2"), key=lambda n: per_launch_ms[n])
+    dk = kernels[dom]
+    bound = "hbm" if dk["hbm_frac"] >= dk["fp32_frac"] else "fp32"
+    return kernels, dom, bound
+
+
+def eager_kernel_times(native, imgs, like, kernel, cfg, N, precision, device, calls):
+    """Per-kernel CUDA-event times from eager calls (each into a fresh output buffer: a new
+    CUDA-graph key, so the call launches kernel by kernel with its events)."""
+    import torch
+    k1 = k2 = 0.0
+    nl = 0
+    fresh = [torch.empty_like(like) for _ in range(calls)]
+    for i, o in enumerate(fresh):
+        st = native.gpa(imgs[i % len(imgs)], o, kernel, cfg.sigma_r, N, 128.0, 128.0, precision, device)
+        k1, k2, nl = k1 + st["k1_ms"], k2 + st["k2_ms"], nl + max(1, st["launches"] // 2)
+    return {"k1": k1 / nl, "k2": k2 / nl}
+
+
+def device_leg(cfg, N, steps, warmup, device, precision, imgs=None):
+    """One rank's device-resident timed steps of a config (inputs in HBM, float32 output), L2
+    flushed between steps when the workload fits L2.  Returns value / timing / roofline."""
+    import torch
+
+    from paper_1603_08109_b200 import _native
+    dev = torch.device("cuda", device)
+    kernel = synth.config_kernel(cfg)
+    if imgs is None:
+        imgs = [torch.from_numpy(im).to(dev) for im in config_images(cfg, range(cfg.batch))]
+    outs = [torch.empty(im.shape, dtype=torch.float32, device=dev) for im in imgs]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if cfg.pixels * 4 <= 126e6 else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if len(imgs) > 1:
+            return _native.gpa_batch(imgs, outs, kernel, cfg.sigma_r, N, 128.0, 128.0, precision, device)
+        return _native.gpa(imgs[0], outs[0], kernel, cfg.sigma_r, N, 128.0, 128.0, precision, device)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    ev, sts = [], []
+    for _ in range(steps):
+        if flush is not None:
+            flush.zero_()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        sts.append(step())
+        b.record(stream)
+        ev.append((a, b))
+    torch.cuda.synchronize(dev)
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    launches = sum(st["launches"] for st in sts) // 2  # per kernel
+    k1 = sum(st["k1_ms"] for st in sts)
+    k2 = sum(st["k2_ms"] for st in sts)
+    if k1 < 0 or k2 < 0 or len(imgs) > 1:
+        # graph replays time only the whole call; a batch overlaps two streams: take the split
+        # from eager one-image calls on one stream outside the timed region
+        per_launch = eager_kernel_times(_native, imgs, outs[0], kernel, cfg, N, precision, device, max(2, steps))
+        split_from = "eager one-image calls outside the timed region"
+    else:
+        per_launch = {"k1": k1 / launches, "k2": k2 / launches}
+        split_from = "timed steps (CUDA events per kernel)"
+    px = sum(int(im.shape[0]) * int(im.shape[1]) for im in imgs)
+    px_per_launch = px * steps / launches
+    kernels, dom, bound = kernel_roofline(cfg, N, per_launch, px_per_launch, launches, ms,
+                                          8 if precision == _native.FB_PREC_F64 else 4)
+    hbm_peak, _ = peaks()
+    bpp = algorithmic_bytes(cfg, N, 8 if precision == _native.FB_PREC_F64 else 4)
+    del outs, flush
+    return {"value": px * steps / (ms * 1e-3) / 1e6, "unit": "MP/s", "ms_per_step": ms / steps, "steps": steps,
+            "warmup": warmup, "ms_total": ms, "launches_per_kernel": launches, "kernels": kernels,
+            "dominant": dom, "bound": bound,
+            "frac": kernels[dom]["hbm_frac"] if bound == "hbm" else kernels[dom]["fp32_frac"],
+            "pipeline_hbm_frac": bpp["pipeline"] * px * steps / (ms * 1e-3) / 1e9 / hbm_peak,
+            "kernel_times_from": split_from, "pixels_per_step": px}
+
+
 def main():
     args = parse()
     cfg = synth.CONFIGS[args.config]
@@ -288,7 +402,7 @@ def main():
     host_ext = None
     if cfg.batch > 1:
         idx = list(sharding.image_shard(cfg.batch, world, rank))
-        host_imgs = [synth.config_image(cfg, i) for i in idx]
+        host_imgs = config_images(cfg, idx)
     else:
         full = synth.config_image(cfg)
         if world > 1 and cfg.name == "c4":
@@ -380,7 +494,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         # row bands (N > 1): each rank's host input is its band plus the halo rows, filtered
-        # through the C ABI with halo_top / halo_bottom, so the band edges are exact
+        # through the C ABI's band entry point (bit-identical rows to a one-GPU call)
         e2e_in = [host_ext] if host_ext is not None else host_imgs
         pinned_in = [torch.from_numpy(im).pin_memory().numpy() for im in e2e_in]
         pinned_out = [torch.empty(im.shape, dtype=torch.float64).pin_memory().numpy() for im in host_imgs]
@@ -424,11 +538,13 @@ def main():
         e2e = {"value": total_px * n_e2e / (float(t_t.item()) * 1e-3) / 1e6, "unit": "MP/s",
                "h2d_bytes_per_step": int(sum(im.nbytes for im in pinned_in)) * world,
                "d2h_bytes_per_step": int(sum(o.nbytes for o in pinned_out)) * world,
+               "calls": n_e2e,
                "path": ("gpa_filter_batch" if len(pinned_in) > 1 else "gpa_filter")
                + "(pinned float32 numpy in, out= pinned float64 numpy): H2D, kernels and D2H pipelined on "
                  "three streams inside the call"
                + ("; at N>1 each rank filters its band from host memory through fb_gpa_filter_band with its "
                   "halo rows (libfbgpu C ABI), output rows to its own pinned buffer" if bands is not None else "")}
+        del pinned_in, pinned_out
 
     if peer is not None:
         dist.barrier()  # teardown: every rank is done with the peer mappings before unmapping
@@ -443,51 +559,20 @@ def main():
     # ---- roofline of the dominant kernel --------------------------------------------------
     hbm_peak, peak_src = peaks()
     bpp = algorithmic_bytes(cfg, N)
-    fpp = algorithmic_flops(cfg, N)
-    calls = max(1, kstats["calls"])
     launches_per_kernel = max(1, kstats["launches"] // 2)
-    px_call = my_pixels / len(host_imgs)
-    kernels = {}
     kernel_times_from = "timed steps (CUDA events per kernel)"
     per_launch = {n: kstats[f"{n}_ms"] / launches_per_kernel for n in ("k1", "k2")}  # ms
-    serial = None
-    if kstats["k1_ms"] < 0 or kstats["k2_ms"] < 0:
-        # small calls replay a CUDA graph (fbgpu.h: k1_ms = k2_ms = -1, only the total is timed):
-        # the per-kernel times come from eager calls outside the timed region (a fresh output
-        # buffer is a new graph key, so those calls launch kernel by kernel with events)
-        serial = "eager calls outside the timed region (the timed steps replay a CUDA graph)"
-    elif len(dev_imgs) > 1:
-        # the timed batch alternates two compute streams, so its per-kernel event spans overlap
-        # and over-count each launch: time the kernels from one-image calls on one stream instead
-        serial = "one-image calls on one stream outside the timed region (the timed batch overlaps two streams)"
-    if serial is not None:
-        k1 = k2 = 0.0
-        nl = 0
-        fresh = [torch.empty_like(dev_out[0]) for _ in range(max(2, args.steps))]  # distinct live buffers
-        for i, o in enumerate(fresh):
-            st = _native.gpa(dev_imgs[i % len(dev_imgs)], o, kernel, cfg.sigma_r, N, 128.0, 128.0,
-                             _native.FB_PREC_F32, local)
-            k1, k2, nl = k1 + st["k1_ms"], k2 + st["k2_ms"], nl + max(1, st["launches"] // 2)
-        del fresh
-        per_launch = {"k1": k1 / nl, "k2": k2 / nl}
-        kernel_times_from = serial
-    for name in ("k1", "k2"):
-        t = per_launch[name] * 1e-3  # s per launch
-        px_launch = my_pixels * args.steps / launches_per_kernel
-        kernels[name] = {
-            "avg_launch_ms": t * 1e3,
-            "share_of_step": per_launch[name] * launches_per_kernel / max(1e-9, ms),
-            "hbm_gbs": bpp[name] * px_launch / t / 1e9,
-            "hbm_frac": bpp[name] * px_launch / t / 1e9 / hbm_peak,
-            "fp32_tflops": fpp[name] * px_launch / t / 1e12,
-            "fp32_frac": fpp[name] * px_launch / t / 1e12 / FP32_NOMINAL_TFLOPS,
-            "alg_bytes_per_px": bpp[name],
-        }
-    dom = max(("k1", "k2"), key=lambda n: per_launch[n])
-    dk = kernels[dom]
-    bound = "hbm" if dk["hbm_frac"] >= dk["fp32_frac"] else "fp32"
-    kname, traffic, traffic_px = ncu_traffic(cfg.name, dom)
+    if kstats["k1_ms"] < 0 or kstats["k2_ms"] < 0 or len(dev_imgs) > 1:
+        # graph replays (fbgpu.h: k1_ms = k2_ms = -1) time only the whole call, and a timed
+        # batch alternates two streams (overlapping per-kernel spans): split from eager
+        # one-image calls on one stream outside the timed region
+        per_launch = eager_kernel_times(_native, dev_imgs, dev_out[0], kernel, cfg, N, _native.FB_PREC_F32,
+                                        local, max(2, args.steps))
+        kernel_times_from = "eager one-image calls outside the timed region"
     px_per_launch = my_pixels * args.steps / launches_per_kernel
+    kernels, dom, bound = kernel_roofline(cfg, N, per_launch, px_per_launch, launches_per_kernel, ms)
+    dk = kernels[dom]
+    kname, traffic, traffic_px = ncu_traffic(cfg.name, dom)
     if traffic is not None and traffic_px and abs(traffic_px - px_per_launch) > 1:
         traffic = traffic * px_per_launch / traffic_px  # profile captured on a different launch size
     roofline = {
@@ -505,6 +590,37 @@ def main():
         "kernels": kernels,
         "kernel_times_from": kernel_times_from,
     }
+
+    # ---- same-precision (fp64) leg and the other configs, device-resident, rank 0, N = 1 ----
+    f64 = per_config = None
+    if world == 1 and not args.no_extra_legs:
+        del dev_out
+        torch.cuda.empty_cache()
+        # the fp64 path (the reference's arithmetic type) on the same inputs
+        leg = device_leg(cfg, N, max(2, min(args.steps, 5)), max(1, min(args.warmup, 2)), local,
+                         _native.FB_PREC_F64, dev_imgs)
+        f64 = {k: leg[k] for k in ("value", "unit", "ms_per_step", "steps", "dominant", "bound", "frac",
+                                   "pipeline_hbm_frac")}
+        f64["dtype"] = "f64"
+        f64["k1_ms"], f64["k2_ms"] = leg["kernels"]["k1"]["avg_launch_ms"], leg["kernels"]["k2"]["avg_launch_ms"]
+        f64["note"] = "precision='f64': fp64 channel planes and arithmetic throughout (8 B per plane value)"
+        del dev_imgs
+        torch.cuda.empty_cache()
+        per_config = {}
+        for name in sorted(synth.CONFIGS):
+            if name == cfg.name:
+                continue
+            c = synth.CONFIGS[name]
+            leg = device_leg(c, synth.config_order(c), args.steps, args.warmup, local, _native.FB_PREC_F32)
+            per_config[name] = {"value": leg["value"], "unit": "MP/s", "ms_per_step": leg["ms_per_step"],
+                                "steps": leg["steps"], "order_N": synth.config_order(c), "dominant": leg["dominant"],
+                                "bound": leg["bound"], "frac": leg["frac"],
+                                "pipeline_hbm_frac": leg["pipeline_hbm_frac"],
+                                "k1_ms": leg["kernels"]["k1"]["avg_launch_ms"],
+                                "k2_ms": leg["kernels"]["k2"]["avg_launch_ms"],
+                                "kernel_times_from": leg["kernel_times_from"],
+                                "config": config_block(c, synth.config_order(c), 1)}
+            torch.cuda.empty_cache()
 
     # ---- CPU baseline (rank 0, N=1 only, bounded sample, one core) ------------------------
     cpu = None
@@ -524,7 +640,7 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (paper_1603_08109_b200/synth.py, seeded; BASELINE recipes)",
         "config": config_block(cfg, N, world), "clocks": clocks.summary(), "gpu_launches": launches,
-        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "f64": f64, "per_config": per_config,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
