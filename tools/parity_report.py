@@ -1,18 +1,25 @@
-"""Full-size parity of the fp32 path: max |delta| per config on the WHOLE image.
+"""Full-size parity: every pixel of every config, GPU paths against the oracle.
 
-The fp64 instantiation of the same kernels is the full-size reference here: it
-matches the reference package's float64 outputs to <= 1e-9 on every golden case
-(tests/test_gpu_parity.py), and the numpy oracle cannot run 268 MP in reasonable
-time.  A few windows per config are additionally checked against the oracle
-itself (interior exactness of the local filter).  Writes profiles/parity_<tag>.json.
+For each config (c0, c1, c2, c4, and all 64 images of c3) the whole workload is filtered by
+  * the fp32 path (the benchmarked one) and the fp64 path, on the GPU;
+  * the oracle (oracle/gpa_oracle.py: the numpy fp64 restatement of the reference, bit-identical
+    to it on the golden cases and on a 1024^2 c4-recipe image), on all host cores in 256 x 2048
+    tiles with W halo rows/columns (the filter is local, so a tile with its halo reproduces the
+    whole-image result on its interior);
+  * the exact O(W^2) bilateral filter (GPU fp64 brute force `bilateral_exact`, pinned to the
+    reference's reference.py:17-45 at 1e-10), to measure the approximation error of our fp32
+    output and of the oracle (= the reference's output) against it.
+Writes profiles/parity_<tag>.json with `pixels_compared` = the full workload.
 
-  python tools/parity_report.py --tag r01 [--configs c0,c1,c2,c3,c4] [--c3-images 4]
+  python tools/parity_report.py --tag r02 [--configs c0,c1,c2,c3,c4]
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import math
+import multiprocessing as mp
 import os
 import sys
 import time
@@ -25,82 +32,104 @@ sys.path.insert(0, ROOT)
 from oracle import gpa_oracle as orc  # noqa: E402  (checker only)
 from paper_1603_08109_b200 import bilateral_exact, gpa_filter, synth  # noqa: E402
 
+_IMG = None  # the image the forked oracle workers read (no per-tile pickling of the input)
+
+
+def _oracle_tile(job):
+    y0, y1, x0, x1, kind, W, taps, sigma_r, N = job
+    H, Wd = _IMG.shape
+    ya, yb, xa, xb = max(0, y0 - W), min(H, y1 + W), max(0, x0 - W), min(Wd, x1 + W)
+    out = orc.gpa(_IMG[ya:yb, xa:xb], kind, W, taps, sigma_r, N)
+    return y0, x0, out[y0 - ya:y1 - ya, x0 - xa:x1 - xa]
+
+
+def oracle_full(img, k, sigma_r, N, pool):
+    """The oracle on the whole image, tiled over the pool (exact: the tiles carry W halos)."""
+    global _IMG
+    _IMG = np.ascontiguousarray(img)
+    H, Wd = img.shape
+    jobs = [(y, min(H, y + 256), x, min(Wd, x + 2048), k.kind, k.half_width, k.weights_1d, sigma_r, N)
+            for y in range(0, H, 256) for x in range(0, Wd, 2048)]
+    out = np.empty((H, Wd), np.float64)
+    for y0, x0, t in pool.imap_unordered(_oracle_tile, jobs, chunksize=1):
+        out[y0:y0 + t.shape[0], x0:x0 + t.shape[1]] = t
+    return out
+
 
 def psnr(mse):
     """20 log10(255) - mse_db (analysis.py:41-46)."""
-    import math
     return math.inf if mse == 0 else 20 * math.log10(255.0) - 10 * math.log10(mse)
 
 
-def window_errs(img, out, k, sigma_r, N, windows):
-    W = k.half_width
-    H, Wd = img.shape
-    worst = 0.0
-    for (y, x, h, w) in windows:
-        y0, x0 = max(0, y - W), max(0, x - W)
-        y1, x1 = min(H, y + h + W), min(Wd, x + w + W)
-        sub = orc.gpa(img[y0:y1, x0:x1], k.kind, W, k.weights_1d, sigma_r, N)
-        ref = sub[y - y0:y - y0 + h, x - x0:x - x0 + w]
-        worst = max(worst, float(np.max(np.abs(out[y:y + h, x:x + w] - ref))))
-    return worst
+class Acc:
+    """max |a - b| (with its location), count above a threshold, sum of squares."""
+
+    def __init__(self):
+        self.max, self.at, self.over, self.ss = 0.0, None, 0, 0.0
+
+    def add(self, a, b, img_index, thr=1e-4):
+        d = np.abs(a - b)
+        j = np.unravel_index(int(np.argmax(d)), d.shape)
+        if d[j] > self.max or self.at is None:
+            self.max, self.at = float(d[j]), [img_index, int(j[0]), int(j[1])]
+        self.over += int((d > thr).sum())
+        self.ss += float(np.sum(d * d))
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--tag", default="r01")
+    ap.add_argument("--tag", default="r02")
     ap.add_argument("--configs", default="c0,c1,c2,c3,c4")
-    ap.add_argument("--c3-images", type=int, default=4)
     args = ap.parse_args()
-    report = {"tag": args.tag, "bar": 1e-3, "configs": {}}
+    report = {"tag": args.tag, "bar": 1e-3, "host_cores": os.cpu_count(), "configs": {},
+              "oracle_tiling": "the oracle runs in 256 x 2048 tiles with W halos; its box sums are global "
+                               "prefix-sum differences (conv.py:30-40), whose rounding depends on where a "
+                               "prefix starts: tiled vs whole-image oracle differ by <= 2.5e-7 on a "
+                               "600 x 2300 c4-recipe image (N = 20), 4000x below the bar"}
+    pool = None
     for name in args.configs.split(","):
         cfg = synth.CONFIGS[name]
         k = synth.config_kernel(cfg)
         N = synth.config_order(cfg)
-        n_img = min(cfg.batch, args.c3_images) if cfg.batch > 1 else 1
-        worst, worst_at, q9999, over1e4, npx = 0.0, None, [], 0, 0
-        approx = {"ours_linf": 0.0, "ref_linf": 0.0, "ours_se": 0.0, "ref_se": 0.0}
         t0 = time.time()
-        for i in range(n_img):
+        f32o, f64o, f32f64 = Acc(), Acc(), Acc()
+        ap32, apref = Acc(), Acc()
+        npx = 0
+        for i in range(cfg.batch):
             img = synth.config_image(cfg, i)
+            if pool is not None:
+                pool.close()
+            global _IMG
+            _IMG = np.ascontiguousarray(img)
+            pool = mp.get_context("fork").Pool(os.cpu_count())
+            ref = oracle_full(img, k, cfg.sigma_r, N, pool)
             o32 = gpa_filter(img, k, cfg.sigma_r, N, precision="f32")
             o64 = gpa_filter(img, k, cfg.sigma_r, N, precision="f64")
+            f32o.add(o32, ref, i)
+            f64o.add(o64, ref, i, thr=1e-9)
+            f32f64.add(o32, o64, i)
             bf = bilateral_exact(img, k, cfg.sigma_r)  # GPU fp64 brute force
-            e32, e64 = np.abs(o32 - bf), np.abs(o64 - bf)
-            approx["ours_linf"] = max(approx["ours_linf"], float(e32.max()))
-            approx["ref_linf"] = max(approx["ref_linf"], float(e64.max()))
-            approx["ours_se"] += float(np.sum(e32 * e32))
-            approx["ref_se"] += float(np.sum(e64 * e64))
-            del bf, e32, e64
-            d = np.abs(o32 - o64)
-            j = np.unravel_index(int(np.argmax(d)), d.shape)
-            if d[j] > worst:
-                worst, worst_at = float(d[j]), [i, int(j[0]), int(j[1]), float(img[j])]
-            q9999.append(float(np.quantile(d, 0.9999)))
-            over1e4 += int((d > 1e-4).sum())
-            npx += d.size
-            H, Wd = img.shape
-            wins = [(0, 0, 40, 40), (H - 40, Wd - 40, 40, 40), (H // 2, Wd // 3, 48, 48)]
-            if worst_at and worst_at[0] == i:
-                y, x = worst_at[1], worst_at[2]
-                wins.append((max(0, y - 8), max(0, x - 8), min(16, H - max(0, y - 8)), min(16, Wd - max(0, x - 8))))
-            w32 = window_errs(img, o32, k, cfg.sigma_r, N, wins)
-            w64 = window_errs(img, o64, k, cfg.sigma_r, N, wins)
-            del o32, o64, d
+            ap32.add(o32, bf, i, thr=math.inf)
+            apref.add(ref, bf, i, thr=math.inf)
+            npx += img.size
+            del ref, o32, o64, bf
         report["configs"][name] = {
-            "images": n_img, "pixels_compared": npx, "order_N": N, "kind": cfg.kind,
+            "images": cfg.batch, "pixels_compared": npx, "order_N": N, "kind": cfg.kind,
             "half_width": k.half_width, "sigma_r": cfg.sigma_r,
-            "max_abs_f32_vs_f64": worst, "worst_pixel": worst_at,
-            "p99.99_abs": max(q9999), "pixels_over_1e-4": over1e4,
-            "windows_max_abs_f32_vs_oracle": w32, "windows_max_abs_f64_vs_oracle": w64,
+            "max_abs_f32_vs_oracle": f32o.max, "worst_pixel_f32": f32o.at,
+            "pixels_f32_over_1e-4": f32o.over, "rms_f32_vs_oracle": math.sqrt(f32o.ss / npx),
+            "max_abs_f64_vs_oracle": f64o.max, "pixels_f64_over_1e-9": f64o.over,
+            "max_abs_f32_vs_f64": f32f64.max,
+            # approximation error vs the exact bilateral filter: our fp32 output and the oracle
+            # (= the reference's gpa_filter output), both over every pixel
+            "approx_linf_ours_f32": ap32.max, "approx_linf_reference": apref.max,
+            "approx_psnr_ours_f32": psnr(ap32.ss / npx), "approx_psnr_reference": psnr(apref.ss / npx),
             "seconds": round(time.time() - t0, 1),
-            # approximation error vs the exact bilateral filter (GPU fp64 brute force): ours (fp32
-            # path) and the reference-equivalent fp64 path (= the reference's gpa_filter to 1e-13)
-            "approx_linf_ours": approx["ours_linf"], "approx_linf_reference": approx["ref_linf"],
-            "approx_psnr_ours": psnr(approx["ours_se"] / npx), "approx_psnr_reference": psnr(approx["ref_se"] / npx),
         }
         print(name, json.dumps(report["configs"][name]), flush=True)
+    if pool is not None:
+        pool.close()
     out = os.path.join(ROOT, "profiles", f"parity_{args.tag}.json")
-    os.makedirs(os.path.dirname(out), exist_ok=True)
     with open(out, "w") as fh:
         json.dump(report, fh, indent=1)
 
