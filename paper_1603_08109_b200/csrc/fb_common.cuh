@@ -89,6 +89,7 @@ struct GpaArgs {
   // the box walker's two-step multipliers q_n = walk_q(n), n < kWalkMaxCh (read as (q_2k, q_2k+1) pairs)
   alignas(8) float walkq[64];
   int walk_rows;      // output rows per thread of the box walker
+  int ch_per_cta;     // kernel 1 tile: channels per CTA (blockIdx.z splits the channels of small images)
 };
 
 // Rows per box walk (kernel 1, both precisions): long walks amortise the 2W warm-up rows; shorter
