@@ -288,3 +288,27 @@ def test_repeated_calls_are_bit_identical(kind, param, sr, n, precision):
     first = outs[0].cpu().numpy()
     for o in outs[1:]:
         assert np.array_equal(o.cpu().numpy(), first)
+
+
+def test_fused_single_pass_prototype_matches(tmp_path):
+    """The single-pass box kernel (fb_fused.cuh, selected by FBGPU_FUSED_BOX=1
+    and read once per process, hence the subprocess) stays within the bar of the fp64 path."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch\n"
+        "from paper_1603_08109_b200 import gpa_filter, make_spatial_kernel, synth\n"
+        "img = synth.config_image('c4', height=2304, width=2048)\n"
+        "k = make_spatial_kernel('box', half_width=20)\n"
+        "d = torch.from_numpy(img).cuda()\n"
+        "st = {}\n"
+        "o32 = gpa_filter(d, k, 25.0, 57, precision='f32', stats=st).cpu().numpy()\n"
+        "o64 = gpa_filter(d, k, 25.0, 57, precision='f64').cpu().numpy()\n"
+        "print(float(np.max(np.abs(o32 - o64))), st['launches'])\n")
+    env = dict(os.environ, FBGPU_FUSED_BOX="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    err, launches = r.stdout.split()
+    assert float(err) <= 1e-3 and int(launches) == 1
