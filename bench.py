@@ -156,8 +156,9 @@ def ncu_traffic(config, stage):
     try:
         with open(path) as fh:
             d = json.load(fh)
+        prefix = {"fused": "k_small"}.get(stage, stage)  # the small-image kernel is k_small_fused
         for name, k in d["kernels"].items():
-            if name.startswith(stage):
+            if name.startswith(prefix):
                 return name, k["dram_bytes_per_launch"], d.get("pixels_per_launch")
     except Exception:
         pass
@@ -285,6 +286,25 @@ def kernel_roofline(cfg, N, per_launch_ms, px_per_launch, launches, step_ms_tota
     bpp = algorithmic_bytes(cfg, N, ch_bytes)
     fpp = algorithmic_flops(cfg, N)
     kernels = {}
+    if per_launch_ms["k2"] <= 0:
+        # small images: one fused kernel (fb_small.cuh), no channel planes in HBM; its algorithmic
+        # bytes are the input and the output only, its flops those of both passes
+        t = per_launch_ms["k1"] * 1e-3
+        s_io = bpp["k1"] + bpp["k2"] - (bpp["pipeline"])  # = s_in (counted twice in k1 + k2)
+        b = bpp["pipeline"] - 2 * (bpp["k1"] - s_io)      # s_in + s_out
+        f = fpp["k1"] + fpp["k2"]
+        kernels["fused"] = {
+            "avg_launch_ms": t * 1e3,
+            "share_of_step": per_launch_ms["k1"] * launches / max(1e-9, step_ms_total),
+            "hbm_gbs": b * px_per_launch / t / 1e9,
+            "hbm_frac": b * px_per_launch / t / 1e9 / hbm_peak,
+            "fp32_tflops": f * px_per_launch / t / 1e12,
+            "fp32_frac": f * px_per_launch / t / 1e12 / FP32_NOMINAL_TFLOPS,
+            "alg_bytes_per_px": b,
+            "two_kernel_alg_bytes_per_px": bpp["pipeline"],
+        }
+        dk = kernels["fused"]
+        return kernels, "fused", "hbm" if dk["hbm_frac"] >= dk["fp32_frac"] else "fp32"
     for name in ("k1", "k2"):
         t = per_launch_ms[name] * 1e-3
         kernels[name] = {
@@ -311,7 +331,7 @@ def eager_kernel_times(native, imgs, like, kernel, cfg, N, precision, device, ca
     fresh = [torch.empty_like(like) for _ in range(calls)]
     for i, o in enumerate(fresh):
         st = native.gpa(imgs[i % len(imgs)], o, kernel, cfg.sigma_r, N, 128.0, 128.0, precision, device)
-        k1, k2, nl = k1 + st["k1_ms"], k2 + st["k2_ms"], nl + max(1, st["launches"] // 2)
+        k1, k2, nl = k1 + st["k1_ms"], k2 + st["k2_ms"], nl + max(1, st["bands"])
     return {"k1": k1 / nl, "k2": k2 / nl}
 
 
@@ -348,7 +368,7 @@ def device_leg(cfg, N, steps, warmup, device, precision, imgs=None):
         ev.append((a, b))
     torch.cuda.synchronize(dev)
     ms = sum(a.elapsed_time(b) for a, b in ev)
-    launches = sum(st["launches"] for st in sts) // 2  # per kernel
+    launches = sum(st["bands"] for st in sts)  # per kernel: one launch of each per row band
     k1 = sum(st["k1_ms"] for st in sts)
     k2 = sum(st["k2_ms"] for st in sts)
     if k1 < 0 or k2 < 0 or len(imgs) > 1:
@@ -436,7 +456,7 @@ def main():
         flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
     ctx_stream = torch.cuda.current_stream(dev)
-    kstats = {"k1_ms": 0.0, "k2_ms": 0.0, "kernel_ms": 0.0, "calls": 0, "launches": 0}
+    kstats = {"k1_ms": 0.0, "k2_ms": 0.0, "kernel_ms": 0.0, "calls": 0, "launches": 0, "bands": 0}
 
     def step(record=False):
         if bands is not None:
@@ -459,6 +479,7 @@ def main():
                 kstats["kernel_ms"] += st["kernel_ms"]
                 kstats["calls"] += 1
                 kstats["launches"] += st["launches"]
+                kstats["bands"] += st["bands"]
 
     def timed(fn, steps):
         ev = []
@@ -559,7 +580,7 @@ def main():
     # ---- roofline of the dominant kernel --------------------------------------------------
     hbm_peak, peak_src = peaks()
     bpp = algorithmic_bytes(cfg, N)
-    launches_per_kernel = max(1, kstats["launches"] // 2)
+    launches_per_kernel = max(1, kstats["bands"])  # one launch of each kernel per row band
     kernel_times_from = "timed steps (CUDA events per kernel)"
     per_launch = {n: kstats[f"{n}_ms"] / launches_per_kernel for n in ("k1", "k2")}  # ms
     if kstats["k1_ms"] < 0 or kstats["k2_ms"] < 0 or len(dev_imgs) > 1:

@@ -303,12 +303,13 @@ int launch_band(fb_ctx* ctx, cudaStream_t st, int kind, GpaArgs<T>& a, int band_
   const int W = a.W;
   bool done = false;
   cudaEvent_t e0 = ctx->next_kev(), e1 = ctx->next_kev(), e2 = ctx->next_kev();
-  KernelEvents kev{e0, e1, e2};
+  int launched = 2;
+  KernelEvents kev{e0, e1, e2, &launched};
   int rc = launch_fast<T>(st, kind, W, a, kev, &done);
   if (rc != FB_OK) return fail(FB_ERR_CUDA, std::string("fast kernel launch failed: ") +
                                                cudaGetErrorString(cudaGetLastError()));
   if (done) {
-    g_launches += 2;
+    g_launches += launched;
     return FB_OK;
   }
   const size_t s1 = generic::k1_smem<T>(W), s2 = generic::k2_smem<T>(W);

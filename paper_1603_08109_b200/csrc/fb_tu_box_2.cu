@@ -1,6 +1,7 @@
 // fb_tu_box_2.cu — specialised fp32 box kernels for half-width group 2 (see fb_fast.cuh);
 // one translation unit per group so the library builds in parallel.
 #include "fb_fast.cuh"
+#include "fb_small.cuh"
 #include "fb_fused.cuh"
 
 namespace fbgpu {

@@ -1,6 +1,7 @@
 // fb_tu_gauss_2.cu — specialised fp32 gauss kernels for half-width group 2 (see fb_fast.cuh);
 // one translation unit per group so the library builds in parallel.
 #include "fb_fast.cuh"
+#include "fb_small.cuh"
 
 namespace fbgpu {
 FB_FAST_DISPATCH(launch_fast_gauss_2, kKindGauss, FB_W_GROUP_2)

@@ -171,7 +171,7 @@ def test_batch_matches_single_and_names_bad_image():
     k = make_spatial_kernel("gaussian", sigma_s=3.0)
     stats = {}
     outs = gpa_filter_batch(imgs, k, 40.0, 15, stats=stats, precision="f32")
-    assert stats["launches"] == 2 * len(imgs)
+    assert stats["launches"] == len(imgs)  # small images: one fused kernel each (fb_small.cuh)
     for im, o in zip(imgs, outs):
         assert np.array_equal(o, gpa_filter(im, k, 40.0, 15, precision="f32"))
     bad = [im.copy() for im in imgs]
