@@ -256,13 +256,17 @@ __global__ void __launch_bounds__(SM_THREADS, sm_min_blocks(WT)) k_small_fused(c
   if (n_nonfinite) atomicAdd(a.flags + kFlagNonfiniteOut, n_nonfinite);
 }
 
-// FBGPU_SMALL_FUSED=0 keeps kernel 1 + kernel 2 for small images (A/B measurements).
-inline bool small_fused_enabled() {
-  static const int on = [] {
+// Which small images take the fused kernel.  Default: Gaussian windows only.  Measured on a B200
+// (tools/small_check.py, tools/diag_latency.py): c0 (Gaussian W = 9, N = 15) 28 us against
+// 20.7 + 15.1 us for kernel 1 + kernel 2 (graph-replayed call 35 against 39-43 us); c1 (box
+// W = 5, N = 10) 43 us against 23.1 + 20.5 us, and its graph-replayed call 55 against 46 us, so
+// box windows keep the two kernels.  FBGPU_SMALL_FUSED=1 fuses both kinds, =0 neither.
+inline bool small_fused_enabled(int kind) {
+  static const int mode = [] {
     const char* e = std::getenv("FBGPU_SMALL_FUSED");
-    return e && *e == '0' ? 0 : 1;
+    return !e || !*e ? -1 : (*e == '0' ? 0 : 1);
   }();
-  return on != 0;
+  return mode < 0 ? kind == kKindGauss : mode != 0;
 }
 
 // Host: one launch for the band (returns 0, or 6 on a launch error).

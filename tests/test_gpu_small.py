@@ -1,6 +1,9 @@
 """GPU parity of the fused small-image kernel (csrc/fb_small.cuh): images of fewer than 2 Mi padded
 samples on the fp32 path run gpa_filter (engine.py:27-80) in one kernel per 32 x 32 tile, the
-channels generated, filtered (conv.py:30-64) and accumulated without leaving the SM.
+channels generated, filtered (conv.py:30-64) and accumulated without leaving the SM.  It is the
+default for Gaussian windows; box windows keep kernel 1 + kernel 2 unless FBGPU_SMALL_FUSED=1
+(read once per process: the box cases of this module run again under it in a subprocess,
+tests/small_fused_cases.py).
 
 Whole images are compared with the oracle (pinned to the reference) and with the fp64 path; band
 calls, batches and the two-kernel path must agree with the whole-image call.
@@ -20,6 +23,11 @@ from paper_1603_08109_b200 import (ParameterError, RangeViolationError, _native,
 pytestmark = pytest.mark.gpu
 
 F32_TOL = 1e-3
+
+
+def _launches(kind):
+    """Kernels per band: the fused kernel for Gaussian windows (and for box windows when forced)."""
+    return 1 if kind == "gaussian" or os.environ.get("FBGPU_SMALL_FUSED") == "1" else 2
 
 
 def _kernel(kind, param):
@@ -44,7 +52,7 @@ def test_small_fused_matches_oracle(h, w, kind, param, sigma_r, N, dtype):
     k = _kernel(kind, param)
     st = {}
     o32 = gpa_filter(img, k, sigma_r, N, precision="f32", stats=st)
-    assert st["launches"] == 1 and st["bands"] == 1  # the fused kernel, not kernel 1 + kernel 2
+    assert st["launches"] == _launches(kind) and st["bands"] == 1
     ref = orc.gpa(img.astype(np.float64), kind, k.half_width, k.weights_1d, sigma_r, N)
     assert np.max(np.abs(o32 - ref)) <= F32_TOL
     o64 = gpa_filter(img, k, sigma_r, N, precision="f64")
@@ -60,7 +68,7 @@ def test_small_configs_every_pixel(name):
     N = synth.config_order(cfg)
     st = {}
     out = gpa_filter(img, k, cfg.sigma_r, N, precision="f32", stats=st)
-    assert st["launches"] == 1
+    assert st["launches"] == _launches(cfg.kind)
     ref = orc.gpa(img.astype(np.float64), cfg.kind, k.half_width, k.weights_1d, cfg.sigma_r, N)
     assert np.max(np.abs(out - ref)) <= 1e-4
 
@@ -87,7 +95,7 @@ def test_small_band_calls_are_bit_identical(kind, param, sigma_r, N):
         below = torch.from_numpy(np.ascontiguousarray(img[r1:r1 + nb])).cuda() if nb else None
         out = torch.empty((r1 - r0, Wd), dtype=torch.float64, device="cuda")
         st = _native.gpa_band(band, out, k, sigma_r, N, 128.0, 128.0, _native.FB_PREC_F32, r0, H, above, below, 0)
-        assert st["launches"] == 1
+        assert st["launches"] == _launches(kind)
         assert np.array_equal(out.cpu().numpy(), full[r0:r1]), (r0, r1)
 
 
@@ -126,28 +134,20 @@ def test_small_validation_names_the_first_offender():
 
 
 def test_small_fused_agrees_with_two_kernels():
-    """FBGPU_SMALL_FUSED=0 (read once per process) keeps kernel 1 + kernel 2 for small images: the
-    same filter to fp32 rounding of the planes."""
-    code = (
-        "import numpy as np\n"
-        "from paper_1603_08109_b200 import gpa_filter, synth\n"
-        "for name in ('c0', 'c1'):\n"
-        "    cfg = synth.CONFIGS[name]\n"
-        "    st = {}\n"
-        "    o = gpa_filter(synth.config_image(cfg), synth.config_kernel(cfg), cfg.sigma_r, synth.config_order(cfg),\n"
-        "                   precision='f32', stats=st)\n"
-        "    np.save(f'{name}.npy', o)\n"
-        "    print(st['launches'])\n")
+    """FBGPU_SMALL_FUSED (read once per process) = 1 fuses box windows too, = 0 keeps kernel 1 +
+    kernel 2 everywhere: the same filter to fp32 rounding of the planes on c0 and c1, and the
+    box cases of this module hold on the fused kernel (tests/small_fused_cases.py)."""
     import tempfile
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = os.path.join(root, "tests", "small_fused_cases.py")
     outs = {}
     for flag, launches in (("1", "1"), ("0", "2")):
         with tempfile.TemporaryDirectory() as tmp:
             env = dict(os.environ, FBGPU_SMALL_FUSED=flag, PYTHONPATH=root)
-            r = subprocess.run([sys.executable, "-c", code], env=env, cwd=tmp, capture_output=True, text=True,
-                               timeout=600)
-            assert r.returncode == 0, r.stderr[-2000:]
-            assert r.stdout.split() == [launches, launches]
+            r = subprocess.run([sys.executable, script], env=env, cwd=tmp, capture_output=True, text=True,
+                               timeout=900)
+            assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-2000:])
+            assert r.stdout.split()[:2] == [launches, launches]
             outs[flag] = [np.load(os.path.join(tmp, f"{n}.npy")) for n in ("c0", "c1")]
     for a, b in zip(outs["1"], outs["0"]):
         assert np.max(np.abs(a - b)) <= 1e-4
