@@ -520,21 +520,25 @@ def main():
         pinned_in = [torch.from_numpy(im).pin_memory().numpy() for im in e2e_in]
         pinned_out = [torch.empty(im.shape, dtype=torch.float64).pin_memory().numpy() for im in host_imgs]
 
+        e2e_st = {}  # the library's own count of the bytes each call moved over PCIe
+
         def e2e_step():
             if len(pinned_in) > 1:
-                gpa_filter_batch(pinned_in, kernel, cfg.sigma_r, N, precision="f32", device=local, outs=pinned_out)
+                gpa_filter_batch(pinned_in, kernel, cfg.sigma_r, N, precision="f32", device=local, outs=pinned_out,
+                                 stats=e2e_st)
             else:
                 if host_ext is not None:
                     top, bottom = bands.halos(rank)
                     r0, r1 = bands.bounds(rank)
                     ext = pinned_in[0]
-                    _native.gpa_band(ext[top:top + r1 - r0], pinned_out[0], kernel, cfg.sigma_r, N, 128.0, 128.0,
-                                     _native.FB_PREC_F32, row_origin=r0, image_rows=cfg.height,
-                                     above=ext[:top] if top else None, below=ext[top + r1 - r0:] if bottom else None,
-                                     device=local)
+                    e2e_st.update(_native.gpa_band(
+                        ext[top:top + r1 - r0], pinned_out[0], kernel, cfg.sigma_r, N, 128.0, 128.0,
+                        _native.FB_PREC_F32, row_origin=r0, image_rows=cfg.height,
+                        above=ext[:top] if top else None, below=ext[top + r1 - r0:] if bottom else None,
+                        device=local))
                 else:
                     gpa_filter(pinned_in[0], kernel, cfg.sigma_r, N, precision="f32", device=local,
-                               out=pinned_out[0])
+                               out=pinned_out[0], stats=e2e_st)
 
         for _ in range(max(1, args.warmup)):  # the device leg's warm-up (small calls turn into
             t_w = time.perf_counter()          # CUDA-graph replays after the first sightings)
@@ -557,12 +561,15 @@ def main():
         if world > 1:
             dist.all_reduce(t_t, op=dist.ReduceOp.MAX)
         e2e = {"value": total_px * n_e2e / (float(t_t.item()) * 1e-3) / 1e6, "unit": "MP/s",
-               "h2d_bytes_per_step": int(sum(im.nbytes for im in pinned_in)) * world,
-               "d2h_bytes_per_step": int(sum(o.nbytes for o in pinned_out)) * world,
+               "h2d_bytes_per_step": int(e2e_st.get("h2d_bytes", sum(im.nbytes for im in pinned_in))) * world,
+               "d2h_bytes_per_step": int(e2e_st.get("d2h_bytes", sum(o.nbytes for o in pinned_out))) * world,
+               "host_out_bytes_per_step": int(sum(o.nbytes for o in pinned_out)) * world,
                "calls": n_e2e,
                "path": ("gpa_filter_batch" if len(pinned_in) > 1 else "gpa_filter")
-               + "(pinned float32 numpy in, out= pinned float64 numpy): H2D, kernels and D2H pipelined on "
-                 "three streams inside the call"
+               + f"(pinned {pinned_in[0].dtype} numpy in, out= pinned float64 numpy): H2D, kernels and D2H pipelined "
+                 "inside the call; byte counts are the library's (calls over 16 MP send the fp32 path's float32 "
+                 "centred result over PCIe and widen it to the float64 output on host threads, "
+                 "csrc/fb_hostwiden.cuh)"
                + ("; at N>1 each rank filters its band from host memory through fb_gpa_filter_band with its "
                   "halo rows (libfbgpu C ABI), output rows to its own pinned buffer" if bands is not None else "")}
         del pinned_in, pinned_out

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -18,6 +19,7 @@
 #include "fb_common.cuh"
 #include "fb_generic.cuh"
 #include "fb_fast.cuh"
+#include "fb_hostwiden.cuh"
 
 namespace fbgpu {
 // ============================================================================ validation
@@ -131,6 +133,15 @@ struct fb_ctx {
   // into graphs: work runs on own_stream, ordered after everything already queued there.
   cudaStream_t upstream = nullptr;
   cudaEvent_t ev_upstream = nullptr;
+  // fp32 path, float64 host output: float32 centred rows cross PCIe and host threads widen them
+  // (fb_hostwiden.cuh).  widen_threads < 0: not configured yet; 0: off.
+  hostwiden::Pool* widen = nullptr;
+  int widen_threads = -1;
+  struct WidenChunk {
+    cudaEvent_t landed;  // recorded after the chunk's device -> staging copy
+    hostwiden::Task task;
+  };
+  std::vector<WidenChunk> widen_chunks;  // the current call's chunks, in copy order
   void clear_graphs() {
     for (auto& kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -363,8 +374,19 @@ struct Item {
   long long o_ld;
   int rows_out;
   int chunks;
+  bool widen;     // float64 host output: the float32 centred result crosses PCIe, host threads widen it
 };
 
+// float32 over PCIe + host widening (fb_hostwiden.cuh) applies to the fp32-precision images of a
+// call whose float64 output lives in host memory, when the call is too large for CUDA-graph replay
+// (kGraphMaxPixels; smaller calls are latency-bound and a replay beats the saved bytes: c2, 16.8 MP,
+// 3.0 ms replayed against 3.9 ms widened).  float64 inputs keep the float64 transfer.
+constexpr long long kGraphMaxPixels = 16ll << 20;  // calls up to 16 MP run as CUDA graphs
+bool widen_applies(fb_ctx* ctx, const fb_image* in, const fb_image* out, int precision, long long call_px) {
+  if (ctx->widen_threads < 0) ctx->widen_threads = hostwiden::configured_threads();
+  return ctx->widen_threads > 0 && precision != FB_PREC_F64 && out && !out->on_device && out->dtype == FB_F64 &&
+         in->dtype != FB_F64 && call_px > kGraphMaxPixels;
+}
 // Copy-in / filter / copy-out for `count` images.  Host-resident images are pipelined in
 // row chunks over three streams: H2D of chunk c+1 || kernels of chunk c || D2H of chunk c-1.
 #ifndef FB_CHUNK_PX
@@ -380,14 +402,21 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
   const bool validate_only = items[0].out == nullptr;
   int band = 0;
   GpaArgs<T> a;
-  int rows_max = 0;
-  for (auto& it : items) rows_max = std::max(rows_max, it.rows_out);
+  auto chunk_rows = [](const Item& o) {
+    int crows = (o.rows_out + o.chunks - 1) / o.chunks;
+    if (o.chunks > 1) crows = (crows + 255) / 256 * 256;  // chunks start at multiples of 256 rows (walk_rows)
+    return crows;
+  };
+  int rows_max = 0;  // rows one launch sequence covers: an image, or one chunk of it
+  for (auto& it : items) rows_max = std::max(rows_max, std::min(it.rows_out, chunk_rows(it)));
   if (!validate_only) {
     int rc = prepare<T>(ctx, j, (int)items[0].in->cols, rows_max, a, &band);
     if (rc != FB_OK) return rc;
   }
   // Batches alternate images between two compute streams with two workspaces, so the kernels
-  // of image i+1 fill the tail waves of image i.
+  // of image i+1 fill the tail waves of image i.  (The chunks of one large host image stay on one
+  // stream: alternating them measured the same, 37.8 against 38.3 ms per c4 call -- that path is
+  // bound by host memory traffic, profiles/r02_hostwiden.md.)
   const bool dual = !validate_only && items.size() > 1;
   cudaStream_t cs[2] = {ctx->stream, dual ? ctx->s_alt : ctx->stream};
   T* wsp[2] = {a.v, a.v};
@@ -415,10 +444,10 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
     Item& it = items[i];
     const fb_image* in = it.in;
     const size_t ies = dtype_size(in->dtype);
-    const int slot = (int)(i & 1);
-    cudaStream_t cstr = cs[slot];
+    const int slot = (int)(i & 1);  // staging buffers of the image
     const bool host_in = !in->on_device;
     const bool host_out = it.out && !it.out->on_device;
+    const bool widen = !validate_only && it.widen;
     // device buffers (double-buffered across images; reuse waits for image i-2)
     if (host_in) {
       int rc = grow(ctx, &ctx->in_stage[slot], &ctx->in_stage_bytes[slot], (size_t)in->rows * in->cols * ies);
@@ -431,13 +460,13 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
       it.f_ld = in->ld;
     }
     if (it.out) {
-      const size_t oes = dtype_size(it.out->dtype);
+      const size_t oes = widen ? sizeof(float) : dtype_size(it.out->dtype);
       if (host_out) {
         int rc = grow(ctx, &ctx->out_stage[slot], &ctx->out_stage_bytes[slot], (size_t)it.rows_out * it.out->cols * oes);
         if (rc != FB_OK) return rc;
         it.o = ctx->out_stage[slot];
         it.o_ld = it.out->cols;
-        if (i >= 2) FB_CUDA(cudaStreamWaitEvent(cstr, out_done[i - 2], 0));
+        if (i >= 2) FB_CUDA(cudaStreamWaitEvent(cs[slot], out_done[i - 2], 0));
       } else {
         it.o = it.out->data;
         it.o_ld = it.out->ld;
@@ -445,12 +474,22 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
     }
     const int W = validate_only ? 0 : j.W;
     const int nch = it.chunks;
-    int crows = (it.rows_out + nch - 1) / nch;
-    if (nch > 1) crows = (crows + 255) / 256 * 256;  // chunks start at multiples of 256 rows (walk_rows)
+    const int crows = chunk_rows(it);
+    size_t stage_off = 0;  // where the image's float32 rows start in the pinned staging area
+    if (widen) {
+      if (!ctx->widen) ctx->widen = new hostwiden::Pool(ctx->widen_threads);
+      size_t total = 0;
+      for (size_t k = 0; k < items.size(); ++k) {
+        if (k == i) stage_off = total;
+        if (items[k].widen) total += (size_t)items[k].rows_out * items[k].out->cols * sizeof(float);
+      }
+      if (ctx->widen_chunks.empty()) FB_CUDA(ctx->widen->reserve(total));  // (no work pending: it may grow)
+    }
     long long copied = 0;  // input buffer rows already sent
     for (int c = 0; c < nch; ++c) {
       const int r0 = c * crows, r1 = std::min(it.rows_out, r0 + crows);
       if (r0 >= r1) break;
+      cudaStream_t cstr = cs[slot];
       if (host_in) {
         // input buffer rows this chunk reads: [halo_top + r0 - W, halo_top + r1 + W) clamped
         const long long need = std::min<long long>(in->rows, (long long)halo_top + r1 + W);
@@ -499,7 +538,7 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
         }
         a.out = it.o;
         a.out_ld = it.o_ld;
-        a.out_dtype = it.out->dtype;
+        a.out_dtype = widen ? (j.mode == kModeGpa ? kOutF32Centred : FB_F32) : it.out->dtype;
         a.flags = ctx->flags + 4 * i;
         a.v = wsp[slot];
         int nb = 0;
@@ -511,17 +550,34 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
         cudaEvent_t e = ctx->next_pev();
         FB_CUDA(cudaEventRecord(e, cstr));
         FB_CUDA(cudaStreamWaitEvent(ctx->s_d2h, e, 0));
-        const size_t oes = dtype_size(it.out->dtype);
-        FB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(it.out->data) + (size_t)r0 * it.out->ld * oes,
-                                  it.out->ld * oes, static_cast<char*>(it.o) + (size_t)r0 * it.o_ld * oes,
-                                  it.o_ld * oes, it.out->cols * oes, r1 - r0, cudaMemcpyDeviceToHost, ctx->s_d2h));
-        if (st) st->d2h_bytes += (long long)(r1 - r0) * it.out->cols * (long long)oes;
+        if (widen) {
+          // float32 rows -> pinned staging; the calling thread hands them to the workers (execute())
+          hostwiden::Task t;
+          t.src = ctx->widen->stage(stage_off + (size_t)r0 * it.out->cols * sizeof(float));
+          t.dst = static_cast<double*>(it.out->data) + (size_t)r0 * it.out->ld;
+          t.rows = r1 - r0;
+          t.cols = it.out->cols;
+          t.dst_ld = it.out->ld;
+          t.add = j.mode == kModeGpa ? j.tc : 0.0;
+          FB_CUDA(cudaMemcpyAsync(const_cast<float*>(t.src), static_cast<char*>(it.o) + (size_t)r0 * it.o_ld * sizeof(float),
+                                  (size_t)(r1 - r0) * it.out->cols * sizeof(float), cudaMemcpyDeviceToHost, ctx->s_d2h));
+          cudaEvent_t landed = ctx->next_pev();
+          FB_CUDA(cudaEventRecord(landed, ctx->s_d2h));
+          ctx->widen_chunks.push_back({landed, t});
+          if (st) st->d2h_bytes += (long long)(r1 - r0) * it.out->cols * (long long)sizeof(float);
+        } else {
+          const size_t oes = dtype_size(it.out->dtype);
+          FB_CUDA(cudaMemcpy2DAsync(static_cast<char*>(it.out->data) + (size_t)r0 * it.out->ld * oes,
+                                    it.out->ld * oes, static_cast<char*>(it.o) + (size_t)r0 * it.o_ld * oes,
+                                    it.o_ld * oes, it.out->cols * oes, r1 - r0, cudaMemcpyDeviceToHost, ctx->s_d2h));
+          if (st) st->d2h_bytes += (long long)(r1 - r0) * it.out->cols * (long long)oes;
+        }
       }
     }
     img_done[i] = ctx->next_pev();
-    FB_CUDA(cudaEventRecord(img_done[i], cstr));
+    FB_CUDA(cudaEventRecord(img_done[i], cs[slot]));
     out_done[i] = ctx->next_pev();
-    FB_CUDA(cudaEventRecord(out_done[i], host_out ? ctx->s_d2h : cstr));
+    FB_CUDA(cudaEventRecord(out_done[i], host_out ? ctx->s_d2h : cs[slot]));
   }
   // join the copy streams and the second compute stream back into the main stream
   cudaEvent_t e1 = ctx->next_pev(), e2 = ctx->next_pev(), e3 = ctx->next_pev();
@@ -570,7 +626,6 @@ int order_after_caller(fb_ctx* ctx) {
 }
 
 // Run `count` images through the pipeline, read the flags back and map them to a status.
-constexpr long long kGraphMaxPixels = 16ll << 20;  // calls up to 16 MP run as CUDA graphs
 
 // Everything the GPU work of a device-resident call depends on: the images (pointers, shapes,
 // strides, dtypes), the filter (incl. taps), precision, halos, the stream and the workspaces.
@@ -614,6 +669,8 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
   }
   ctx->kev_used = 0;
   ctx->pev_used = 0;
+  ctx->widen_chunks.clear();
+  const long long t_call0 = hostwiden::Pool::now_ns();
   if ((rc = order_after_caller(ctx)) != FB_OK) return rc;
   FB_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
   std::vector<Item> items(count);
@@ -634,6 +691,16 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
     nch = std::max<long long>(1, std::min<long long>(nch, it.rows_out / 256));
     // (batches overlap image i+1's copies with image i's kernels instead: no chunks)
     it.chunks = (count == 1 && host_io && px >= (4ll << 20) && it.rows_out >= 512) ? (int)nch : 1;
+  }
+  bool any_widen = false;
+  size_t widen_bytes = 0;
+  for (auto& it : items) {
+    any_widen |= it.widen = widen_applies(ctx, it.in, it.out, precision, pixels);
+    if (it.widen) widen_bytes += (size_t)it.rows_out * it.in->cols * sizeof(float);
+  }
+  if (widen_bytes > hostwiden::max_stage_bytes()) {  // the pinned staging holds the call's whole float32 output
+    any_widen = false;
+    for (auto& it : items) it.widen = false;
   }
   const long long launches0 = g_launches.load();
   unsigned long long* fl_all = ctx->flags_host + 4 * ctx->flags_cap;
@@ -667,6 +734,7 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
   };
   bool replay_ok = ctx->use_graphs && pixels <= kGraphMaxPixels && (outs == nullptr || ctx->tab_n == j.N);
   for (auto& it : items) replay_ok = replay_ok && replayable(it.in) && (!it.out || replayable(it.out));
+  replay_ok = replay_ok && !any_widen;  // (host functions and ring slots stay out of graphs)
   fb_ctx::Graph* g = nullptr;
   if (replay_ok) {
     std::string key = graph_key(ctx, ins, outs, count, halo_top, halo_bottom, j, precision, geo);
@@ -716,7 +784,20 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
   if (!g) FB_CUDA(cudaEventRecord(ctx->ev_kend, ctx->stream));
   FB_CUDA(cudaEventRecord(ctx->ev_end, ctx->stream));
   const bool replayed = g != nullptr;
-  FB_CUDA(cudaEventSynchronize(ctx->ev_end));
+  // Hand the float32 chunks to the host threads as they land (nothing is submitted before this
+  // point, so the early returns above leave no host work behind), then wait for the rest.
+  for (auto& wc : ctx->widen_chunks) {
+    if (cudaEventSynchronize(wc.landed) != cudaSuccess) break;  // (the error surfaces below)
+    ctx->widen->submit(wc.task);
+  }
+  const cudaError_t sync_err = cudaEventSynchronize(ctx->ev_end);
+  if (ctx->widen && !ctx->widen_chunks.empty()) ctx->widen->wait_all();
+  FB_CUDA(sync_err);
+  if (ctx->widen && !ctx->widen_chunks.empty()) {
+    const long long t_sync = hostwiden::Pool::now_ns();
+    static const bool trace = std::getenv("FBGPU_WIDEN_TRACE") != nullptr;
+    if (trace) ctx->widen->trace_report(t_call0, t_sync, hostwiden::Pool::now_ns());
+  }
   local.launches = g_launches.load() - launches0;
   local.precision = precision;
 
@@ -762,17 +843,32 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
       status = fail(FB_ERR_NUMERIC, "non-finite output");
     }
   }
+  if (any_widen && status == FB_OK && local.degenerate_pixels > 0) {
+    // A pixel under the Q floor returns the input sample itself (engine.py:68), which the centred
+    // float32 transfer may not carry exactly: repeat the call with float64 rows over PCIe.
+    const int saved = ctx->widen_threads;
+    ctx->widen_threads = 0;
+    const int rr = execute(ctx, ins, outs, count, halo_top, halo_bottom, j, precision, st, geo);
+    ctx->widen_threads = saved;
+    return rr;
+  }
   float ms = 0.f, kms = 0.f;
   cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_end);
   if (!replayed) cudaEventElapsedTime(&kms, ctx->ev_kstart, ctx->ev_kend);
   local.device_ms = ms;
   local.kernel_ms = replayed ? ms : kms;  // a replayed graph is timed as a whole
+  static const bool trace_bands = std::getenv("FBGPU_TRACE_BANDS") != nullptr;
   for (int b = 0; b + 2 < ctx->kev_used; b += 3) {
     float t1 = 0.f, t2 = 0.f;
     cudaEventElapsedTime(&t1, ctx->kev[b], ctx->kev[b + 1]);
     cudaEventElapsedTime(&t2, ctx->kev[b + 1], ctx->kev[b + 2]);
     local.k1_ms += t1;
     local.k2_ms += t2;
+    if (trace_bands) {  // where each band's kernels sit in the call (ms after the call's first event)
+      float t0 = 0.f;
+      cudaEventElapsedTime(&t0, ctx->ev_start, ctx->kev[b]);
+      fprintf(stderr, "[band %d] k1 start +%.3f  k1 %.3f  k2 %.3f  end +%.3f\n", b / 3, t0, t1, t2, t0 + t1 + t2);
+    }
   }
   if (replayed) local.k1_ms = local.k2_ms = -1.0;  // graph call: only kernel_ms (the total) exists
   local.spatial_filter_calls = j.N + 1;
@@ -920,6 +1016,8 @@ int fb_destroy(fb_ctx* c) {
   cudaSetDevice(c->device);
   if (c->own_stream) cudaStreamSynchronize(c->own_stream);
   c->clear_graphs();
+  delete c->widen;  // joins the host threads, frees the pinned staging area
+  c->widen = nullptr;
   for (void* p : {c->ws, c->ws2, c->in_stage[0], c->in_stage[1], c->out_stage[0], c->out_stage[1], (void*)c->flags,
                   (void*)c->tab, (void*)c->tabd})
     if (p) cudaFree(p);

@@ -71,7 +71,7 @@ struct GpaArgs {
   // output
   void* out;
   long long out_ld;
-  int out_dtype;      // 0 u8 (quantised as save_pgm does), 1 f32, 2 f64
+  int out_dtype;      // 0 u8 (quantised as save_pgm does), 1 f32, 2 f64, 3 f32 holding result - tc (kOutF32Centred)
   unsigned long long* flags;
   // fp32 channel constants, 4 per channel m: r_m = fl32(1/sqrt(m)) (0 for m = 0), sqrt(m),
   // and the matched Horner constants h_m = 1/(m r_m), s_m = 1/r_m rounded to fp32
@@ -139,9 +139,20 @@ __device__ __forceinline__ unsigned quantize_u8(double v) {
   return (unsigned)floor(fmin(fmax(v, 0.0), 255.0) + 0.5);
 }
 
-__device__ __forceinline__ void store_sample(void* out, int dt, long long idx, double v) {
+// Results of the fp32 path: the centred result sigma_r P/Q is rounded to float32 once, in the
+// epilogue, and t_c is added in fp64 (f32_result).  Its accuracy is fp32; with the
+// rounding made explicit, a float64 host output can cross PCIe as the float32 centred result
+// (out_dtype kOutF32Centred) and be widened on the host, result = (double)r + t_c, to the very bits
+// the float64 device output holds (fb_hostwiden.cuh).  Rounding the CENTRED value keeps the
+// reference's shift commutation (test_acceptance.py:130-143) exact on this path too.
+constexpr int kOutF32Centred = 3;
+__device__ __forceinline__ double f32_result(double centred, double tc) { return (double)(float)centred + tc; }
+
+// `tc` matters for kOutF32Centred only.
+__device__ __forceinline__ void store_sample(void* out, int dt, long long idx, double v, double tc = 0.0) {
   if (dt == 2) reinterpret_cast<double*>(out)[idx] = v;
   else if (dt == 1) reinterpret_cast<float*>(out)[idx] = (float)v;
+  else if (dt == kOutF32Centred) reinterpret_cast<float*>(out)[idx] = (float)(v - tc);
   else reinterpret_cast<unsigned char*>(out)[idx] = (unsigned char)quantize_u8(v);
 }
 

@@ -239,13 +239,13 @@ __global__ void __launch_bounds__(FU_THREADS, 1) k_fused_box(const __grid_consta
       fph ^= 1u;
     }
     if (!col_ok) continue;
-    double o = a.sr * ddiv_newton(u, q) + a.tc;
+    double o = f32_result(a.sr * ddiv_newton(u, q), a.tc);
     if (fabs(q * (double)a.norm) < 1e-30) {  // Q floor (engine.py:20, 68)
       o = fv;
       ++n_degenerate;
     }
     n_nonfinite += !isfinite(o);
-    store_sample(a.out, a.out_dtype, (long long)(a.band_row0 + orow) * a.out_ld + col, o);
+    store_sample(a.out, a.out_dtype, (long long)(a.band_row0 + orow) * a.out_ld + col, o, a.tc);
   }
   if (n_degenerate) atomicAdd(a.flags + kFlagDegenerate, n_degenerate);
   if (n_nonfinite) atomicAdd(a.flags + kFlagNonfiniteOut, n_nonfinite);

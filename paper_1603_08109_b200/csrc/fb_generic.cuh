@@ -17,6 +17,7 @@
 //     so q_0 = Q and p_0 = P of engine.py:60-66 exactly; then
 //     out = sigma_r * P/Q + t_c, with the |Q| < 1e-30 pass-through (engine.py:68-72).
 #pragma once
+#include <type_traits>
 #include "fb_common.cuh"
 
 namespace fbgpu {
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(256) k2_hpass_horner(const GpaArgs<T> a) {
     const int col = x0 + c0 + j;
     double o;
     if (a.mode == kModePlain) {
-      o = (double)(hv[j] * a.norm);
+      o = (double)(hv[j] * a.norm);  // (T = float: already an fp32 value)
     } else {
       const T qn = q[j] * a.norm;
       if (fabs((double)qn) < 1e-30) {
@@ -184,11 +185,11 @@ __global__ void __launch_bounds__(256) k2_hpass_horner(const GpaArgs<T> a) {
         atomicAdd(a.flags + kFlagDegenerate, 1ull);
       } else {
         const T ratio = (T)a.sr * (p[j] / q[j]);
-        o = (double)ratio + a.tc;
+        o = (double)ratio + a.tc;  // (T = float: an fp32 centred result + t_c, as f32_result)
       }
     }
     if (!isfinite(o)) atomicAdd(a.flags + kFlagNonfiniteOut, 1ull);
-    store_sample(a.out, a.out_dtype, (long long)(a.band_row0 + orow) * a.out_ld + col, o);
+    store_sample(a.out, a.out_dtype, (long long)(a.band_row0 + orow) * a.out_ld + col, o, a.tc);
   }
 }
 

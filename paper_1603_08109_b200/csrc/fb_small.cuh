@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(SM_THREADS, sm_min_blocks(WT)) k_small_fused(c
   unsigned long long n_degenerate = 0, n_nonfinite = 0;
 #pragma unroll
   for (int j = 0; j < SM_RH; ++j) {
-    o[j] = a.sr * ddiv_newton(pd[j], qd[j]) + a.tc;
+    o[j] = f32_result(a.sr * ddiv_newton(pd[j], qd[j]), a.tc);
     if (fabs(qd[j] * (double)a.norm) < 1e-30) {  // Q floor (engine.py:20, 68)
       o[j] = fown[j];
       n_degenerate += col0 + j < a.cols;
@@ -243,14 +243,15 @@ __global__ void __launch_bounds__(SM_THREADS, sm_min_blocks(WT)) k_small_fused(c
     double2* p = reinterpret_cast<double2*>(reinterpret_cast<double*>(a.out) + oidx);
     p[0] = make_double2(o[0], o[1]);
     p[1] = make_double2(o[2], o[3]);
-  } else if (a.out_dtype == 1 && col0 + SM_RH <= a.cols &&
+  } else if ((a.out_dtype == 1 || a.out_dtype == kOutF32Centred) && col0 + SM_RH <= a.cols &&
              (reinterpret_cast<uintptr_t>(reinterpret_cast<float*>(a.out) + oidx) & 15) == 0) {
+    const double sub = a.out_dtype == kOutF32Centred ? a.tc : 0.0;
     *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + oidx) =
-        make_float4((float)o[0], (float)o[1], (float)o[2], (float)o[3]);
+        make_float4((float)(o[0] - sub), (float)(o[1] - sub), (float)(o[2] - sub), (float)(o[3] - sub));
   } else {
 #pragma unroll
     for (int j = 0; j < SM_RH; ++j)
-      if (col0 + j < a.cols) store_sample(a.out, a.out_dtype, oidx + j, o[j]);
+      if (col0 + j < a.cols) store_sample(a.out, a.out_dtype, oidx + j, o[j], a.tc);
   }
   if (n_degenerate) atomicAdd(a.flags + kFlagDegenerate, n_degenerate);
   if (n_nonfinite) atomicAdd(a.flags + kFlagNonfiniteOut, n_nonfinite);
