@@ -137,11 +137,7 @@ struct fb_ctx {
   // (fb_hostwiden.cuh).  widen_threads < 0: not configured yet; 0: off.
   hostwiden::Pool* widen = nullptr;
   int widen_threads = -1;
-  struct WidenChunk {
-    cudaEvent_t landed;  // recorded after the chunk's device -> staging copy
-    hostwiden::Task task;
-  };
-  std::vector<WidenChunk> widen_chunks;  // the current call's chunks, in copy order
+  bool widen_used = false;  // the current call dispatched pieces to the host threads
   void clear_graphs() {
     for (auto& kv : graphs)
       if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -242,8 +238,8 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
     const int cap = std::max(j.N + 1, 256);
     FB_CUDA(cudaMalloc(&ctx->tab, 4 * sizeof(float) * cap));
     FB_CUDA(cudaMallocHost(&ctx->tab_host, 4 * sizeof(float) * cap));
-    FB_CUDA(cudaMalloc(&ctx->tabd, 4 * sizeof(double) * cap));  // [sequential | walker] sections
-    FB_CUDA(cudaMallocHost(&ctx->tabd_host, 4 * sizeof(double) * cap));
+    FB_CUDA(cudaMalloc(&ctx->tabd, 6 * sizeof(double) * cap));  // [sequential | walker | tile] sections
+    FB_CUDA(cudaMallocHost(&ctx->tabd_host, 6 * sizeof(double) * cap));
     ctx->tab_cap = cap;
   }
   if (ctx->tab_n != j.N) {
@@ -278,15 +274,24 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
       wd[2 * m] = h;
       wd[2 * m + 1] = sg;
     }
+    // ... and for planes made by the fp32 tile kernel 1, whose every order is multiplied by kappa
+    double* td = ctx->tabd_host + 4 * ctx->tab_cap;
+    const double kap = (double)tile_kappa(j.N);
+    for (int m = 0; m <= j.N; ++m) {
+      td[2 * m] = m > 0 ? 1.0 / ((double)m * kap) : 0.0;
+      td[2 * m + 1] = m > 0 ? 1.0 / kap : 0.0;
+    }
     FB_CUDA(cudaMemcpyAsync(ctx->tab, ctx->tab_host, 4 * sizeof(float) * (j.N + 1), cudaMemcpyHostToDevice,
                             ctx->stream));
-    FB_CUDA(cudaMemcpyAsync(ctx->tabd, ctx->tabd_host, 4 * sizeof(double) * ctx->tab_cap, cudaMemcpyHostToDevice,
+    FB_CUDA(cudaMemcpyAsync(ctx->tabd, ctx->tabd_host, 6 * sizeof(double) * ctx->tab_cap, cudaMemcpyHostToDevice,
                             ctx->stream));
     ctx->tab_n = j.N;
   }
   a.tab = ctx->tab;
   a.tabd = a.tabd_seq = ctx->tabd;
   a.tabd_walk = ctx->tabd + 2 * ctx->tab_cap;
+  a.tabd_tile = ctx->tabd + 4 * ctx->tab_cap;
+  a.kappa = tile_kappa(j.N);
   a.wpad = cols + 2 * j.W;
   a.pitch = (a.wpad + 31) / 32 * 32;
   // Row bands: the N+1 planes of one band must fit under the workspace limit.
@@ -477,13 +482,13 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
     const int crows = chunk_rows(it);
     size_t stage_off = 0;  // where the image's float32 rows start in the pinned staging area
     if (widen) {
-      if (!ctx->widen) ctx->widen = new hostwiden::Pool(ctx->widen_threads);
+      if (!ctx->widen) ctx->widen = new hostwiden::Pool(ctx->widen_threads, ctx->device);
       size_t total = 0;
       for (size_t k = 0; k < items.size(); ++k) {
         if (k == i) stage_off = total;
         if (items[k].widen) total += (size_t)items[k].rows_out * items[k].out->cols * sizeof(float);
       }
-      if (ctx->widen_chunks.empty()) FB_CUDA(ctx->widen->reserve(total));  // (no work pending: it may grow)
+      if (!ctx->widen_used) FB_CUDA(ctx->widen->reserve(total));  // (no work pending: it may grow)
     }
     long long copied = 0;  // input buffer rows already sent
     for (int c = 0; c < nch; ++c) {
@@ -551,19 +556,25 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
         FB_CUDA(cudaEventRecord(e, cstr));
         FB_CUDA(cudaStreamWaitEvent(ctx->s_d2h, e, 0));
         if (widen) {
-          // float32 rows -> pinned staging; the calling thread hands them to the workers (execute())
-          hostwiden::Task t;
-          t.src = ctx->widen->stage(stage_off + (size_t)r0 * it.out->cols * sizeof(float));
-          t.dst = static_cast<double*>(it.out->data) + (size_t)r0 * it.out->ld;
-          t.rows = r1 - r0;
-          t.cols = it.out->cols;
-          t.dst_ld = it.out->ld;
-          t.add = j.mode == kModeGpa ? j.tc : 0.0;
-          FB_CUDA(cudaMemcpyAsync(const_cast<float*>(t.src), static_cast<char*>(it.o) + (size_t)r0 * it.o_ld * sizeof(float),
-                                  (size_t)(r1 - r0) * it.out->cols * sizeof(float), cudaMemcpyDeviceToHost, ctx->s_d2h));
-          cudaEvent_t landed = ctx->next_pev();
-          FB_CUDA(cudaEventRecord(landed, ctx->s_d2h));
-          ctx->widen_chunks.push_back({landed, t});
+          // float32 rows -> pinned staging, in pieces; the dispatcher hands each to the workers as it lands
+          const size_t row_bytes = (size_t)it.out->cols * sizeof(float);
+          const int prow = (int)std::max<size_t>(1, hostwiden::piece_bytes() / row_bytes);
+          for (int p0 = r0; p0 < r1; p0 += prow) {
+            const int p1 = std::min(r1, p0 + prow);
+            hostwiden::Task t;
+            t.src = ctx->widen->stage(stage_off + (size_t)p0 * row_bytes);
+            t.dst = static_cast<double*>(it.out->data) + (size_t)p0 * it.out->ld;
+            t.rows = p1 - p0;
+            t.cols = it.out->cols;
+            t.dst_ld = it.out->ld;
+            t.add = j.mode == kModeGpa ? j.tc : 0.0;
+            FB_CUDA(cudaMemcpyAsync(const_cast<float*>(t.src), static_cast<char*>(it.o) + (size_t)p0 * it.o_ld * sizeof(float),
+                                    (size_t)(p1 - p0) * row_bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
+            cudaEvent_t landed = ctx->next_pev();
+            FB_CUDA(cudaEventRecord(landed, ctx->s_d2h));
+            ctx->widen->dispatch(landed, t);
+            ctx->widen_used = true;
+          }
           if (st) st->d2h_bytes += (long long)(r1 - r0) * it.out->cols * (long long)sizeof(float);
         } else {
           const size_t oes = dtype_size(it.out->dtype);
@@ -669,8 +680,15 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
   }
   ctx->kev_used = 0;
   ctx->pev_used = 0;
-  ctx->widen_chunks.clear();
+  ctx->widen_used = false;
   const long long t_call0 = hostwiden::Pool::now_ns();
+  // Whatever path leaves this function, the host threads are done with the caller's output first.
+  struct WidenDrain {
+    fb_ctx* c;
+    ~WidenDrain() {
+      if (c->widen_used) c->widen->wait_all();
+    }
+  } widen_drain{ctx};
   if ((rc = order_after_caller(ctx)) != FB_OK) return rc;
   FB_CUDA(cudaEventRecord(ctx->ev_start, ctx->stream));
   std::vector<Item> items(count);
@@ -784,16 +802,10 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
   if (!g) FB_CUDA(cudaEventRecord(ctx->ev_kend, ctx->stream));
   FB_CUDA(cudaEventRecord(ctx->ev_end, ctx->stream));
   const bool replayed = g != nullptr;
-  // Hand the float32 chunks to the host threads as they land (nothing is submitted before this
-  // point, so the early returns above leave no host work behind), then wait for the rest.
-  for (auto& wc : ctx->widen_chunks) {
-    if (cudaEventSynchronize(wc.landed) != cudaSuccess) break;  // (the error surfaces below)
-    ctx->widen->submit(wc.task);
-  }
   const cudaError_t sync_err = cudaEventSynchronize(ctx->ev_end);
-  if (ctx->widen && !ctx->widen_chunks.empty()) ctx->widen->wait_all();
+  if (ctx->widen_used) ctx->widen->wait_all();  // the host threads are done with the caller's output
   FB_CUDA(sync_err);
-  if (ctx->widen && !ctx->widen_chunks.empty()) {
+  if (ctx->widen_used) {
     const long long t_sync = hostwiden::Pool::now_ns();
     static const bool trace = std::getenv("FBGPU_WIDEN_TRACE") != nullptr;
     if (trace) ctx->widen->trace_report(t_call0, t_sync, hostwiden::Pool::now_ns());

@@ -79,9 +79,14 @@ struct GpaArgs {
   // fp64 Horner constants matched to r_m (see k2f_hpass_horner): tabd[2m] = 1/(m r_m), tabd[2m+1] = 1/r_m.
   // tabd is the set matching the kernel that made the planes: tabd_seq (c_m = c_{m-1} x r_m) or
   // tabd_walk (the box walker's two-step recurrence, r_m replaced by its effective ratio).
+  // tabd_tile: the fp32 tile kernel 1 (k1f_gen_vpass) multiplies every order by the same constant,
+  // c_m = c_{m-1} (x kappa), r_m = kappa = fl32(1/sqrt(N)): one multiply per sample and channel
+  // instead of two, no per-channel constant load (see fb_fast.cuh).
   const double* tabd;
   const double* tabd_seq;
   const double* tabd_walk;
+  const double* tabd_tile;
+  float kappa;
   T w[kMaxTaps];      // normalised 1-D taps (gaussian)
   // Tap pairs for packed FFMA2 (fp32 fast path): wq[2a] = w[a], wq[2a+1] = w[a-1],
   // a = 0 .. 2W+1, with w[-1] = w[2W+1] = 0 (box: all ones).
@@ -117,6 +122,12 @@ __device__ __forceinline__ long long sample_row(const GpaArgs<T>& a, long long b
   return b < a.halo_top ? a.top_off + b * a.top_ld
                         : (b < a.main_end ? b * a.f_ld : a.bot_off + (b - a.main_end) * a.bot_ld);
 }
+
+// The fp32 tile kernel 1's channel scale: channel m = e^{-x^2/2} (kappa x)^m with kappa =
+// fl32(1/sqrt(N)).  Its largest value over x, at x = sqrt(m), is e^{(m/2)(ln(m/N) - 1)} <= 1 for
+// every m <= N, so no order overflows whatever sigma_r is; the fp64 Horner constants (tabd_tile)
+// undo kappa^m exactly as they undo the 1/sqrt(m!) of the other kernels.
+inline float tile_kappa(int N) { return (float)(1.0 / std::sqrt((double)(N > 1 ? N : 1))); }
 
 constexpr int kWalkMaxCh = 64;              // channels (N+1) the register-resident box walker holds
 

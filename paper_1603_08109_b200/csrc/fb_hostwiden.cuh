@@ -7,12 +7,12 @@
 // float64 device output holds (fb_common.cuh: f32_result) -- while the next chunks are in flight.  For c4 that halves the D2H bytes (2 GiB -> 1 GiB per 16384^2 image),
 // which is what bounded the end-to-end rate (profiles/r01_pcie_probe.txt).
 //
-// Protocol: every chunk's float32 rows go device -> their place in a pinned staging area that holds
-// the whole call's float32 output (no slot reuse, so the copy stream never waits for the host);
-// an event follows each copy.  The calling thread, which would otherwise sleep until the call's
-// last event, waits for the chunk events in order and hands each chunk to the workers.  (A first
-// version used cudaLaunchHostFunc hand-offs and a six-slot ring: two host functions per chunk
-// put ~0.7 ms of dispatch latency per chunk on the copy stream, 41 ms per c4 call.)
+// Protocol: the float32 rows go device -> their place in a pinned staging area that holds the whole
+// call's float32 output (no slot reuse, so the copy stream never waits for the host), in pieces of
+// a few MiB with an event after each.  A dispatcher thread waits for the piece events in order and
+// hands each piece to the workers.  (A first version used cudaLaunchHostFunc hand-offs and a
+// six-slot ring: two host functions per chunk put ~0.7 ms of dispatch latency per chunk on the
+// copy stream, 41 ms per c4 call.)
 #pragma once
 #include <cuda_runtime.h>
 #include <immintrin.h>
@@ -72,8 +72,9 @@ struct Task {
 
 class Pool {
  public:
-  explicit Pool(int threads) : fn_(pick_widen()) {
+  Pool(int threads, int device) : fn_(pick_widen()), device_(device) {
     for (int t = 0; t < threads; ++t) workers_.emplace_back([this] { run(); });
+    dispatcher_ = std::thread([this] { dispatch_loop(); });
   }
   ~Pool() {
     {
@@ -81,7 +82,9 @@ class Pool {
       stop_ = true;
     }
     cv_work_.notify_all();
+    cv_disp_.notify_all();
     for (auto& w : workers_) w.join();
+    dispatcher_.join();
     if (stage_) cudaFreeHost(stage_);
   }
   int threads() const { return (int)workers_.size(); }
@@ -100,13 +103,23 @@ class Pool {
   }
   float* stage(size_t byte_offset) const { return reinterpret_cast<float*>(stage_ + byte_offset); }
 
-  // a chunk has landed in the staging area: split its rows over the workers
+  // `landed` has been recorded after the copy of the piece: widen it once the event completes
+  void dispatch(cudaEvent_t landed, const Task& t) {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      dq_.push_back({landed, t});
+      ++pending_;  // the piece itself, until its parts are queued
+    }
+    cv_disp_.notify_one();
+  }
+  // a piece has landed in the staging area: split its rows over the workers
   void submit(const Task& t) {
     if (trace_first_ == 0) trace_first_ = now_ns();
     const int parts = (int)std::max<long long>(1, std::min<long long>(threads(), t.rows));
     const long long per = (t.rows + parts - 1) / parts;
     {
       std::lock_guard<std::mutex> lk(m_);
+      --pending_;
       for (long long r = 0; r < t.rows; r += per) {
         Task p = t;
         p.src = t.src + r * t.cols;
@@ -119,7 +132,7 @@ class Pool {
     }
     cv_work_.notify_all();
   }
-  // every submitted piece is done
+  // every dispatched piece is widened
   void wait_all() {
     std::unique_lock<std::mutex> lk(m_);
     cv_done_.wait(lk, [&] { return pending_ == 0; });
@@ -139,6 +152,29 @@ class Pool {
   }
 
  private:
+  void dispatch_loop() {
+    cudaSetDevice(device_);
+    for (;;) {
+      std::pair<cudaEvent_t, Task> d;
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_disp_.wait(lk, [&] { return stop_ || !dq_.empty(); });
+        if (dq_.empty()) return;
+        d = dq_.front();
+        dq_.pop_front();
+      }
+      if (cudaEventSynchronize(d.first) == cudaSuccess) {
+        submit(d.second);
+      } else {  // the call fails with the same error at its own synchronisation
+        bool last;
+        {
+          std::lock_guard<std::mutex> lk(m_);
+          last = --pending_ == 0;
+        }
+        if (last) cv_done_.notify_all();
+      }
+    }
+  }
   void run() {
     for (;;) {
       Task t;
@@ -169,8 +205,11 @@ class Pool {
   widen_fn fn_;
   std::vector<std::thread> workers_;
   std::mutex m_;
-  std::condition_variable cv_work_, cv_done_;
+  std::condition_variable cv_work_, cv_done_, cv_disp_;
   std::deque<Task> q_;
+  std::deque<std::pair<cudaEvent_t, Task>> dq_;
+  std::thread dispatcher_;
+  int device_ = 0;
   long long pending_ = 0;
   bool stop_ = false;
   long long trace_first_ = 0, trace_last_ = 0, trace_busy_ = 0, trace_wait_ = 0, trace_pieces_ = 0;
@@ -199,6 +238,20 @@ inline size_t max_stage_bytes() {
   static const size_t v = [] {
     const char* e = std::getenv("FBGPU_WIDEN_MAX_MB");
     return (size_t)(e ? std::max(0, atoi(e)) : 4096) << 20;
+  }();
+  return v;
+}
+}  // namespace hostwiden
+}  // namespace fbgpu
+
+namespace fbgpu {
+namespace hostwiden {
+// Bytes per device -> staging copy (FBGPU_WIDEN_PIECE_KB, default 8192: 32 / 8 / 2 / 1 / 0.5 MiB pieces
+// measured 38.6 / 36.6 / 37.8 / 38.6 / 43.8 ms per c4 call).
+inline size_t piece_bytes() {
+  static const size_t v = [] {
+    const char* e = std::getenv("FBGPU_WIDEN_PIECE_KB");
+    return (size_t)(e ? std::max(64, atoi(e)) : 8192) << 10;
   }();
   return v;
 }
