@@ -223,7 +223,29 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
   // Box walker multipliers: it steps each channel parity by two orders at once,
   // c_n = c_{n-2} * x^2 * q_n with q_n = fl32(1/sqrt((n-1) n)) (q_1 = 1: c_1 = c_0 x), so the
   // even and odd chains are independent (read as (q_2k, q_2k+1) pairs for packed multiplies).
-  for (int m = 0; m < kWalkMaxCh; ++m) a.walkq[m] = walk_q(m);
+  for (int m = 0; m < kWalkMaxCh; ++m) a.walkq[m] = walk_q(m);  // (the fused prototype's walker, fb_fused.cuh)
+  // The production walker: channel m = e^{-x^2/2} (x / s)^m / m!  (fb_common.cuh: taylor_scale)
+  a.walk_xs = (float)(1.0 / taylor_scale(j.N));
+  a.taylor_s = 1.0 / (double)a.walk_xs;
+  // Two-step multipliers q_n ~ 1 / ((n-1) n), each chosen so that the product the walker really
+  // applies, A_n = q_n A_{n-2} (fp32 constants, exact products), is the fp32-nearest to 1/n!:
+  // the constants' representation errors do not accumulate along the chain, every order is within
+  // one fp32 rounding (6e-8) of its Taylor weight, the noise floor of the fp32 planes themselves.
+  // (Plain fl32(1/((n-1) n)) drifts by ~n/2 roundings: over 5e-4 gray levels at c4 against the fp64
+  // path, 2.7e-4 with these constants -- the level of the 1/sqrt(n!) planes with exact fp64 compensation.)
+  {
+    double A[kWalkMaxCh], fact = 1.0;
+    for (int m = 0; m < kWalkMaxCh; ++m) {
+      if (m >= 1) fact *= (double)m;
+      if (m < 2) {
+        a.walkt[m] = 1.f;
+        A[m] = 1.0;
+      } else {
+        a.walkt[m] = (float)((1.0 / fact) / A[m - 2]);
+        A[m] = A[m - 2] * (double)a.walkt[m];
+      }
+    }
+  }
   // channel constants 1/sqrt(m), sqrt(m) (rounded once from double), uploaded when N changes
   if (j.N + 1 > ctx->tab_cap) {
     ctx->realloc_seen = true;

@@ -93,6 +93,13 @@ struct GpaArgs {
   alignas(8) float wq[2 * (2 * kFastMaxW + 2)];
   // the box walker's two-step multipliers q_n = walk_q(n), n < kWalkMaxCh (read as (q_2k, q_2k+1) pairs)
   alignas(8) float walkq[64];
+  // The production walker's "Taylor" normalisation (fb_fast.cuh, k1f_box_walk): channel m =
+  // e^{-x^2/2} xt^m / m! with xt = x / taylor_s, so kernel 2 needs no per-channel constant:
+  // Q = sum_m plane_m y^m with y = x taylor_s, and P = dQ/dx comes from the same Horner pass
+  // (two fp64 FMAs per pixel and channel instead of four fp64 operations).
+  alignas(8) float walkt[64];  // two-step multipliers 1 / ((n-1) n), walkt[0] = walkt[1] = 1
+  float walk_xs;               // 1 / taylor_s (fp32)
+  double taylor_s;             // fp64 value of the fp32 scale the walker divided by
   int walk_rows;      // output rows per thread of the box walker
   int ch_per_cta;     // kernel 1 tile: channels per CTA (blockIdx.z splits the channels of small images)
 };
@@ -128,6 +135,16 @@ __device__ __forceinline__ long long sample_row(const GpaArgs<T>& a, long long b
 // every m <= N, so no order overflows whatever sigma_r is; the fp64 Horner constants (tabd_tile)
 // undo kappa^m exactly as they undo the 1/sqrt(m!) of the other kernels.
 inline float tile_kappa(int N) { return (float)(1.0 / std::sqrt((double)(N > 1 ? N : 1))); }
+
+// Scale of the Taylor normalisation: the largest value of channel m, at x = sqrt(m), is
+// e^{(m/2) ln(N/m) - m ln(beta)} for s = sqrt(e/N) beta: at most e^{N/(2 e beta^2)}, and 1 at m = N.
+// beta = max(1, sqrt(N/326)) keeps every order under e^60 in fp32 whatever sigma_r is (beta = 1 for
+// the walker's N <= 63: at most e^{11.6}).
+inline double taylor_scale(int N) {
+  const double n = (double)(N > 1 ? N : 1);
+  const double beta = n > 326.0 ? std::sqrt(n / 326.0) : 1.0;
+  return std::sqrt(2.718281828459045 / n) * beta;
+}
 
 constexpr int kWalkMaxCh = 64;              // channels (N+1) the register-resident box walker holds
 
