@@ -400,7 +400,9 @@ struct Item {
   void* o;        // device output
   long long o_ld;
   int rows_out;
-  int chunks;
+  int chunks;     // > 1: a host image pipelined in row chunks
+  int crows;      // most rows a chunk has
+  std::vector<int> ends;  // last row + 1 of every chunk (multiples of 256 but the last)
   bool widen;     // float64 host output: the float32 centred result crosses PCIe, host threads widen it
 };
 
@@ -429,13 +431,8 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
   const bool validate_only = items[0].out == nullptr;
   int band = 0;
   GpaArgs<T> a;
-  auto chunk_rows = [](const Item& o) {
-    int crows = (o.rows_out + o.chunks - 1) / o.chunks;
-    if (o.chunks > 1) crows = (crows + 255) / 256 * 256;  // chunks start at multiples of 256 rows (walk_rows)
-    return crows;
-  };
   int rows_max = 0;  // rows one launch sequence covers: an image, or one chunk of it
-  for (auto& it : items) rows_max = std::max(rows_max, std::min(it.rows_out, chunk_rows(it)));
+  for (auto& it : items) rows_max = std::max(rows_max, std::min(it.rows_out, it.crows));
   if (!validate_only) {
     int rc = prepare<T>(ctx, j, (int)items[0].in->cols, rows_max, a, &band);
     if (rc != FB_OK) return rc;
@@ -500,8 +497,6 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
       }
     }
     const int W = validate_only ? 0 : j.W;
-    const int nch = it.chunks;
-    const int crows = chunk_rows(it);
     size_t stage_off = 0;  // where the image's float32 rows start in the pinned staging area
     if (widen) {
       if (!ctx->widen) ctx->widen = new hostwiden::Pool(ctx->widen_threads, ctx->device);
@@ -513,9 +508,9 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
       if (!ctx->widen_used) FB_CUDA(ctx->widen->reserve(total));  // (no work pending: it may grow)
     }
     long long copied = 0;  // input buffer rows already sent
-    for (int c = 0; c < nch; ++c) {
-      const int r0 = c * crows, r1 = std::min(it.rows_out, r0 + crows);
-      if (r0 >= r1) break;
+    int r0 = 0;
+    for (size_t ci = 0; ci < it.ends.size(); r0 = it.ends[ci], ++ci) {
+      const int r1 = it.ends[ci];
       cudaStream_t cstr = cs[slot];
       if (host_in) {
         // input buffer rows this chunk reads: [halo_top + r0 - W, halo_top + r1 + W) clamped
@@ -717,7 +712,7 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
   long long pixels = 0;
   for (int i = 0; i < count; ++i) {
     Item& it = items[i];
-    memset(&it, 0, sizeof(it));
+    it = Item{};
     it.in = ins + i;
     it.out = outs ? outs + i : nullptr;
     it.rows_out = (int)(geo.separate() ? ins[i].rows : ins[i].rows - halo_top - halo_bottom);
@@ -731,6 +726,69 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
     nch = std::max<long long>(1, std::min<long long>(nch, it.rows_out / 256));
     // (batches overlap image i+1's copies with image i's kernels instead: no chunks)
     it.chunks = (count == 1 && host_io && px >= (4ll << 20) && it.rows_out >= 512) ? (int)nch : 1;
+    it.crows = it.rows_out;
+    std::vector<long long> sizes;  // rows of the chunks, in order
+    if (it.chunks > 1) {
+      it.crows = (it.rows_out + it.chunks - 1) / it.chunks;
+      it.crows = (it.crows + 255) / 256 * 256;  // chunks start at multiples of 256 rows (walk_rows)
+      // The fp32 box walker runs one CTA per 128 columns and walk, two per SM: a 512-row c4 chunk is
+      // 258 CTAs for 296 slots, and kernel 1 took 0.48 ms per 512 rows against 0.37 ms inside a
+      // 4096-row band.  Its chunks are sized in walks so that the grid fills whole waves (c4: 9
+      // walks = 2304 rows = 3.92 waves), ramping up from short chunks that start the pipeline
+      // (each sized so its copy lands while the chunks before it are filtered) and down to short
+      // ones at the end (the last chunk's copy-out and widening are not overlapped by kernels).
+      const long long cols = ins[i].cols, wpad = cols + 2 * j.W;
+      const long long image_rows = geo.image_rows > 0 ? geo.image_rows : it.rows_out;
+      if (precision != FB_PREC_F64 && j.kind == FB_BOX && j.W <= kFastMaxW && j.N + 1 <= kWalkMaxCh &&
+          wpad * image_rows >= (4ll << 20)) {
+        const long long walk = walk_rows((int)wpad, (int)image_rows, 128);
+        const long long gx = (wpad + 127) / 128, slots = 2ll * ctx->sm_count;
+        const long long w_lo = std::max<long long>(1, (FB_CHUNK_PX + cols * walk - 1) / (cols * walk));
+        const long long w_hi = std::max<long long>(w_lo, (5 * FB_CHUNK_PX) / (cols * walk));
+        long long best = w_lo;
+        double best_eff = 0.0;
+        for (long long w = w_lo; w <= w_hi; ++w) {
+          const double waves = (double)(gx * w) / (double)slots;
+          const double eff = waves / std::ceil(waves);
+          if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = w;
+          }
+        }
+        long long rem = it.rows_out;
+        auto take = [&](long long rows) {
+          rows = std::min(rows, rem);
+          if (rows > 0) {
+            sizes.push_back(rows);
+            rem -= rows;
+          }
+        };
+        long long down_sum = 0;
+        for (long long d : {2 * w_lo, w_lo})
+          if (d < best) down_sum += d * walk;
+        for (long long u : {w_lo, 2 * w_lo, 3 * w_lo})
+          if (u < best && rem > down_sum + (u + best) * walk) take(u * walk);
+        if (rem > down_sum) {  // the middle: chunks of ~best walks, the walks spread evenly over them
+          const long long mid = (rem - down_sum + walk - 1) / walk;
+          const long long n_main = std::max<long long>(1, (mid + best / 2) / best);
+          for (long long k = 0; k < n_main; ++k) take(((mid * (k + 1)) / n_main - (mid * k) / n_main) * walk);
+        }
+        for (long long d : {2 * w_lo, w_lo})
+          if (d < best) take(d * walk);
+        take(rem);
+      } else {
+        for (long long r = 0; r < it.rows_out; r += it.crows) sizes.push_back(std::min<long long>(it.crows, it.rows_out - r));
+      }
+    } else {
+      sizes.push_back(it.rows_out);
+    }
+    long long end = 0;
+    it.crows = 0;
+    for (long long sz : sizes) {
+      end += sz;
+      it.ends.push_back((int)end);
+      it.crows = std::max(it.crows, (int)sz);
+    }
   }
   bool any_widen = false;
   size_t widen_bytes = 0;

@@ -218,13 +218,14 @@ class Pool {
 };
 
 // Host-thread count: FBGPU_HOST_THREADS, else the hardware threads less two (the caller's and the
-// CUDA runtime's), capped at 8 (6, 10 and 14 threads measured the same 38 ms per c4 call on a
-// 16-core host: the path is bound by host memory traffic); 0 disables the float32 transfer
-// (float64 rows cross PCIe instead).
+// CUDA runtime's), capped at 16.  While the GPU side bounded the call, 6, 10 and 14 threads
+// measured the same; with wave-sized chunks the threads bound it: 4 / 8 / 14 threads = 44.0 / 35.7 /
+// 33.4 ms per c4 call on a 16-core host (profiles/r02_hostwiden.md).  0 disables the float32
+// transfer (float64 rows cross PCIe instead).
 inline int configured_threads() {
   if (const char* e = std::getenv("FBGPU_HOST_THREADS")) return std::max(0, std::min(64, atoi(e)));
   const int hw = (int)std::thread::hardware_concurrency();
-  return std::max(1, std::min(8, hw - 2));
+  return std::max(1, std::min(16, hw - 2));
 }
 
 }  // namespace hostwiden
