@@ -498,14 +498,9 @@ int run_items(fb_ctx* ctx, std::vector<Item>& items, int halo_top, int halo_bott
     }
     const int W = validate_only ? 0 : j.W;
     size_t stage_off = 0;  // where the image's float32 rows start in the pinned staging area
-    if (widen) {
-      if (!ctx->widen) ctx->widen = new hostwiden::Pool(ctx->widen_threads, ctx->device);
-      size_t total = 0;
-      for (size_t k = 0; k < items.size(); ++k) {
-        if (k == i) stage_off = total;
-        if (items[k].widen) total += (size_t)items[k].rows_out * items[k].out->cols * sizeof(float);
-      }
-      if (!ctx->widen_used) FB_CUDA(ctx->widen->reserve(total));  // (no work pending: it may grow)
+    if (widen) {  // (execute() reserved the staging area for the whole call)
+      for (size_t k = 0; k < i; ++k)
+        if (items[k].widen) stage_off += (size_t)items[k].rows_out * items[k].out->cols * sizeof(float);
     }
     long long copied = 0;  // input buffer rows already sent
     int r0 = 0;
@@ -796,9 +791,21 @@ int execute(fb_ctx* ctx, const fb_image* ins, fb_image* outs, int count, int hal
     any_widen |= it.widen = widen_applies(ctx, it.in, it.out, precision, pixels);
     if (it.widen) widen_bytes += (size_t)it.rows_out * it.in->cols * sizeof(float);
   }
-  if (widen_bytes > hostwiden::max_stage_bytes()) {  // the pinned staging holds the call's whole float32 output
-    any_widen = false;
-    for (auto& it : items) it.widen = false;
+  if (any_widen) {
+    // the pinned staging holds the call's whole float32 output; without it (over the limit, or the
+    // host refuses to pin that much) the call sends float64 rows instead
+    bool ok = widen_bytes <= hostwiden::max_stage_bytes();
+    if (ok) {
+      if (!ctx->widen) ctx->widen = new hostwiden::Pool(ctx->widen_threads, ctx->device);
+      if (ctx->widen->reserve(widen_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        ok = false;
+      }
+    }
+    if (!ok) {
+      any_widen = false;
+      for (auto& it : items) it.widen = false;
+    }
   }
   const long long launches0 = g_launches.load();
   unsigned long long* fl_all = ctx->flags_host + 4 * ctx->flags_cap;

@@ -89,11 +89,15 @@ def test_host_threads_zero_disables_the_float32_transfer():
         "print(st['d2h_bytes'])\n")
     import tempfile
     outs = {}
-    for threads in ("0", "3"):
+    # (threads, staging limit in MB) -> bytes per pixel over PCIe: no threads or no room for the
+    # pinned staging area mean float64 rows
+    for key, env_add, bpp in (("off", {"FBGPU_HOST_THREADS": "0"}, 8), ("on", {"FBGPU_HOST_THREADS": "3"}, 4),
+                              ("no_room", {"FBGPU_HOST_THREADS": "3", "FBGPU_WIDEN_MAX_MB": "1"}, 8)):
         with tempfile.TemporaryDirectory() as tmp:
-            env = dict(os.environ, FBGPU_HOST_THREADS=threads, PYTHONPATH=ROOT)
+            env = dict(os.environ, PYTHONPATH=ROOT, **env_add)
             r = subprocess.run([sys.executable, "-c", code], env=env, cwd=tmp, capture_output=True, text=True, timeout=600)
             assert r.returncode == 0, r.stderr[-2000:]
-            assert int(r.stdout.split()[-1]) == 4200 * 4100 * (8 if threads == "0" else 4)
-            outs[threads] = np.load(os.path.join(tmp, "o.npy"))
-    assert np.array_equal(outs["0"], outs["3"])
+            assert int(r.stdout.split()[-1]) == 4200 * 4100 * bpp, key
+            outs[key] = np.load(os.path.join(tmp, "o.npy"))
+    assert np.array_equal(outs["off"], outs["on"])
+    assert np.array_equal(outs["off"], outs["no_room"])
