@@ -126,6 +126,11 @@ int fb_set_workspace_limit(fb_ctx* ctx, int64_t bytes);
  * still works, serialised).  The result does not depend on the chunking, the
  * workspace banding or the stream: every output is bit-identical to the one a
  * single device-resident call computes.
+ * The fp32 precision's results are float32 values (the centred result sigma_r P/Q is rounded
+ * to float32 once, then the centre is added in fp64), whatever the output dtype.  A float64 output
+ * in host memory of a call over 16 MP therefore crosses PCIe as float32 and is widened into `out`
+ * by host threads owned by the context (FBGPU_HOST_THREADS; fb_stats.d2h_bytes counts the bytes
+ * that crossed) -- the same bits as a device-resident call.
  * `out` may be FB_F64 (the reference's float64 result), FB_F32, or FB_U8: the 8-bit raster that
  * save_pgm / save_image write (image.py:96-99, :122-127), quantised as floor(clip(v, 0, 255) + 0.5)
  * in kernel 2's epilogue, so a PGM/PNG pipeline moves 1 byte per pixel each way.
