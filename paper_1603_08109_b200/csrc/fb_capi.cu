@@ -260,8 +260,8 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
     const int cap = std::max(j.N + 1, 256);
     FB_CUDA(cudaMalloc(&ctx->tab, 4 * sizeof(float) * cap));
     FB_CUDA(cudaMallocHost(&ctx->tab_host, 4 * sizeof(float) * cap));
-    FB_CUDA(cudaMalloc(&ctx->tabd, 6 * sizeof(double) * cap));  // [sequential | walker | tile] sections
-    FB_CUDA(cudaMallocHost(&ctx->tabd_host, 6 * sizeof(double) * cap));
+    FB_CUDA(cudaMalloc(&ctx->tabd, 7 * sizeof(double) * cap));  // [sequential | walker | tile | Taylor r] sections
+    FB_CUDA(cudaMallocHost(&ctx->tabd_host, 7 * sizeof(double) * cap));
     ctx->tab_cap = cap;
   }
   if (ctx->tab_n != j.N) {
@@ -305,7 +305,11 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
     }
     FB_CUDA(cudaMemcpyAsync(ctx->tab, ctx->tab_host, 4 * sizeof(float) * (j.N + 1), cudaMemcpyHostToDevice,
                             ctx->stream));
-    FB_CUDA(cudaMemcpyAsync(ctx->tabd, ctx->tabd_host, 6 * sizeof(double) * ctx->tab_cap, cudaMemcpyHostToDevice,
+    // ... and the per-order factors of the fp64 kernels' Taylor planes
+    double* tr = ctx->tabd_host + 6 * ctx->tab_cap;
+    const double ts = 1.0 / (double)(float)(1.0 / taylor_scale(j.N));  // = GpaArgs::taylor_s below
+    for (int m = 0; m <= j.N; ++m) tr[m] = m > 0 ? 1.0 / ((double)m * ts) : 0.0;
+    FB_CUDA(cudaMemcpyAsync(ctx->tabd, ctx->tabd_host, 7 * sizeof(double) * ctx->tab_cap, cudaMemcpyHostToDevice,
                             ctx->stream));
     ctx->tab_n = j.N;
   }
@@ -313,6 +317,7 @@ int prepare(fb_ctx* ctx, const Job& j, int cols, int rows_out_max, GpaArgs<T>& a
   a.tabd = a.tabd_seq = ctx->tabd;
   a.tabd_walk = ctx->tabd + 2 * ctx->tab_cap;
   a.tabd_tile = ctx->tabd + 4 * ctx->tab_cap;
+  a.taylor_r = ctx->tabd + 6 * ctx->tab_cap;
   a.kappa = tile_kappa(j.N);
   a.wpad = cols + 2 * j.W;
   a.pitch = (a.wpad + 31) / 32 * 32;

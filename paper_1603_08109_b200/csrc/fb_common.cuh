@@ -100,6 +100,9 @@ struct GpaArgs {
   alignas(8) float walkt[64];  // two-step multipliers 1 / ((n-1) n), walkt[0] = walkt[1] = 1
   float walk_xs;               // 1 / taylor_s (fp32)
   double taylor_s;             // fp64 value of the fp32 scale the walker divided by
+  // fp64 kernels (fb_fast64.cuh): every kernel 1 writes Taylor planes, c_m = c_{m-1} (x taylor_r[m])
+  // with taylor_r[m] = 1 / (m taylor_s) in fp64 (their rounding, ~m 1e-16, is far below the path's 1e-9)
+  const double* taylor_r;
   int walk_rows;      // output rows per thread of the box walker
   int ch_per_cta;     // kernel 1 tile: channels per CTA (blockIdx.z splits the channels of small images)
 };

@@ -11,8 +11,9 @@
 //                                 streams fp64 channel tiles m = N..0 through a TMA/mbarrier
 //                                 ring; horizontal pass + fp64 Horner (no conversions).
 //
-// The channels use the fp32-rounded constants r_m of the fp32 path (tab), so kernel 2's
-// constants tabd (h_m = 1/(m r_m)) cancel the normalisation exactly, as in fb_fast.cuh.
+// Both kernel 1 variants write Taylor planes, c_m = e^{-x^2/2} (x/s)^m / m! (per-order factors
+// taylor_r[m] = 1/(m s) in fp64), so kernel 2 gets Q and P = dQ/dx from one derivative-Horner pass
+// with two FMAs per pixel and channel and no constants (fb_fast.cuh, TAYLOR).
 #pragma once
 #include "fb_fast.cuh"
 
@@ -48,8 +49,8 @@ __global__ void __launch_bounds__(KD_THREADS) k1d_box_walk(const __grid_constant
     return brow < 0 ? 0 : (brow >= a.rows_in ? a.rows_in - 1 : brow);
   };
   auto to_x = [&](double v) -> double { return a.mode == kModeGpa ? (v - a.tc) * a.inv_sr : v; };
-  __shared__ double rn[NCH];  // r_n as used by the fp32 path (tab), promoted; read as broadcasts
-  for (int n = threadIdx.x; n < NCH; n += KD_THREADS) rn[n] = (n >= 1 && n <= N) ? (double)__ldg(a.tab + 4 * n) : 0.0;
+  __shared__ double rn[NCH];  // the Taylor planes' per-order factors 1 / (n s); read as broadcasts
+  for (int n = threadIdx.x; n < NCH; n += KD_THREADS) rn[n] = (n >= 1 && n <= N) ? __ldg(a.taylor_r + n) : 0.0;
   __syncthreads();
   const int steps = rows_here + 2 * W;
   double S[NCH];
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(KT_THREADS) k1d_gen_vpass(const __grid_constan
   double* vp = a.v + (long long)(o0 + ob) * a.rstride + pc;
   for (int n = 0; n <= a.N; ++n, vp += a.pitch) {
     double* cs = (n & 1) ? buf1 : buf0;
-    const double rs = n > 0 ? (double)__ldg(a.tab + 4 * n) : 1.0;
+    const double rs = n > 0 ? __ldg(a.taylor_r + n) : 1.0;  // Taylor planes: c_n = c_{n-1} x / (n s)
 #pragma unroll
     for (int t = 0; t < NS; ++t) {
       const int i = g + KT_RG * t;
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(KD2_THREADS, kd2_ctas<KIND>())
 #pragma unroll
   for (int j = 0; j < KD2_R; ++j) {
     const double fv = (row_ok && col0 + j < a.cols) ? load_sample(a.f, a.f_dtype, brow * a.f_ld + col0 + j) : 0.0;
-    xd[j] = (fv - a.tc) * a.inv_sr;
+    xd[j] = (fv - a.tc) * a.inv_sr * a.taylor_s;  // y = x s: Q = sum_m plane_m y^m (fb_fast.cuh, TAYLOR)
     pd[j] = 0.0;
     qd[j] = 0.0;
   }
@@ -381,38 +382,51 @@ __global__ void __launch_bounds__(KD2_THREADS, kd2_ctas<KIND>())
       }
     }
   };
-  // the Horner recurrences of fb_fast.cuh (q_m = Cbar_m + t q_{m+1}, u_{m-1} = m Cbar_m + t u_m)
-  auto horner = [&](int m, const double* hv, auto DoQ, auto DoU) {
-    constexpr bool kQ = decltype(DoQ)::value, kU = decltype(DoU)::value;
-    const double hm = kQ ? __ldg(a.tabd + 2 * (m + 1)) : 0.0;
-    const double sm = (double)m;
+  // The derivative Horner of fb_fast.cuh on Taylor planes c_m = Fbar_m / (m! s^m), y = x s:
+  //   channel N:      d = N c_N, q = 0          channel N-1:   q = c_{N-1}  (d keeps N c_N)
+  //   channel m < N-1: d <- q + y d,  q <- c_m + y q            (pd holds d);   Q = q, P = s d
+  auto taylor_top = [&](const double* hv) {
+#pragma unroll
+    for (int j = 0; j < KD2_R; ++j) pd[j] = (double)N * hv[j];
+  };
+  auto taylor_first = [&](const double* hv) {
+#pragma unroll
+    for (int j = 0; j < KD2_R; ++j) qd[j] = hv[j];
+  };
+  auto taylor_step = [&](const double* hv) {
 #pragma unroll
     for (int j = 0; j < KD2_R; ++j) {
-      const double t = xd[j] * hm;
-      if constexpr (kQ) qd[j] = fma(t, qd[j], hv[j]);
-      if constexpr (kU) pd[j] = fma(t, pd[j], sm * hv[j]);
+      pd[j] = fma(xd[j], pd[j], qd[j]);
+      qd[j] = fma(xd[j], qd[j], hv[j]);
     }
   };
-  using T_ = std::true_type;
-  using F_ = std::false_type;
 
   double hv[KD2_R], hn[KD2_R];
   load_window(0);
-  hpass(0, hv);
+  hpass(0, hv);  // channel N
   if (N >= 1 && a.mode == kModeGpa) {
     load_window(1);
-    horner(N, hv, F_{}, T_{});
-    hpass(1, hn);
+    taylor_top(hv);
+    hpass(1, hn);  // channel N - 1
 #pragma unroll
     for (int j = 0; j < KD2_R; ++j) hv[j] = hn[j];
-    for (int m = N - 1; m >= 1; --m) {
-      load_window(N - m + 1);
-      horner(m, hv, T_{}, T_{});
-      hpass(N - m + 1, hn);
+    if (N >= 2) {
+      load_window(2);
+      taylor_first(hv);
+      hpass(2, hn);  // channel N - 2
 #pragma unroll
       for (int j = 0; j < KD2_R; ++j) hv[j] = hn[j];
+      for (int m = N - 2; m >= 1; --m) {
+        load_window(N - m + 1);
+        taylor_step(hv);
+        hpass(N - m + 1, hn);  // channel m - 1
+#pragma unroll
+        for (int j = 0; j < KD2_R; ++j) hv[j] = hn[j];
+      }
+      taylor_step(hv);  // channel 0
+    } else {
+      taylor_first(hv);  // N = 1: channel 0
     }
-    horner(0, hv, T_{}, F_{});
   }
 
   // epilogue (as fb_fast.cuh): quotients, Q floor (engine.py:20, 68), bookkeeping, stores
@@ -425,7 +439,7 @@ __global__ void __launch_bounds__(KD2_THREADS, kd2_ctas<KIND>())
     if (a.mode == kModePlain) {
       o[j] = hv[j] * a.norm;
     } else {
-      o[j] = a.sr * (pd[j] / qd[j]) + a.tc;
+      o[j] = a.sr * (pd[j] * a.taylor_s / qd[j]) + a.tc;
       if (fabs(qd[j] * a.norm) < 1e-30) degenerate |= 1u << j;
     }
   }
@@ -465,7 +479,6 @@ inline int make_plane_map64(CUtensorMap* map, const GpaArgs<double>& a, int W) {
 template <int KIND, int WT>
 int launch_pair64(cudaStream_t st, GpaArgs<double>& a, const KernelEvents& ev) {
   const int W = a.W;
-  a.tabd = a.tabd_seq;  // both kernel 1 variants use the sequential recurrence
   void (*k1)(const GpaArgs<double>) = k1d_gen_vpass<KIND, WT>;
   size_t s1 = kt_smem_bytes(W);
   a.lead = KIND == kKindBox ? box_lead(a, KT_RB) : 0;
