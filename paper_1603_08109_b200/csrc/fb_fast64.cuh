@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(KD_THREADS) k1d_box_walk(const __grid_constant
       double* dst = vp + (long long)out_row * a.rstride;
 #pragma unroll
       for (int n = 0; n < NCH; ++n, dst += a.pitch)
-        if (n < NCH - 8 || n <= N) *dst = S[n];
+        if (n < NCH - 8 || n <= N) __stcs(dst, S[n]);  // evict-first: planes are read again only a band later
     }
   }
   if (a.check) {
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(KT_THREADS) k1d_gen_vpass(const __grid_constan
     if (col_ok) {
 #pragma unroll
       for (int r = 0; r < KT_R; ++r)
-        if (o0 + ob + r < a.band_rows && o0 + ob + r >= 0) vp[(long long)r * a.rstride] = acc[r];
+        if (o0 + ob + r < a.band_rows && o0 + ob + r >= 0) __stcs(vp + (long long)r * a.rstride, acc[r]);
     }
   }
 }
