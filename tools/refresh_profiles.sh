@@ -12,9 +12,11 @@ for c in c0 c1 c2; do
   FBGPU_NO_GRAPHS=1 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $R/launches_$c.csv python bench.py --config $c --steps 2 --warmup 1 $B > /dev/null 2>&1
 done
 ncu --set full --clock-control none --import-source on -k regex:"k1f|k2f" -s 2 -c 2 -o $R/prof_c4 python tools/prof_driver.py --config c4 --rows 4096 > /dev/null 2>&1
-for c in c0 c1 c2 c3; do
+for c in c1 c2 c3; do
   FBGPU_NO_GRAPHS=1 ncu --set full --clock-control none --import-source on -k regex:"k1f|k2f" -s 2 -c 2 -o $R/prof_$c python tools/prof_driver.py --config $c > /dev/null 2>&1
 done
+# c0 runs the fused small-image kernel: one launch per call
+FBGPU_NO_GRAPHS=1 ncu --set full --clock-control none --import-source on -k regex:"k_small" -s 1 -c 1 -o $R/prof_c0 python tools/prof_driver.py --config c0 --reps 3 > /dev/null 2>&1
 ls -la $R
 # summaries (small files; the .ncu-rep captures stay on the box except c4's)
 for c in c0 c1 c2 c3 c4; do
